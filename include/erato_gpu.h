@@ -1,0 +1,149 @@
+/* erato_gpu.h — C ABI of the B200-native segmented odd-only sieve.
+ *
+ * Drop-in for the reference sieve path `run_sieve` of erato
+ * (/root/reference/proj/include/erato/driver.hpp:91, src/driver.cpp:83-120).
+ * The reference exposes a C++ API, not an FFI; each entry point below names
+ * the reference interface it replaces.  INTEGRATION.md shows the binding a
+ * maintainer would add on the reference side.
+ *
+ * Conventions
+ *  - Plain C types only; no torch, no CUDA types in the signatures.
+ *  - Return value: 0 on success, else 1 + the ordinal of erato::errc
+ *    (/root/reference/proj/include/erato/params.hpp:18-29), so the same
+ *    codes/names (L_OUT_OF_RANGE, F_ZERO_OR_OVERLAP, ...) come back.
+ *    Parameter errors are codes 1..5 (CLI exit 1), runtime errors 6..
+ *    (CLI exit 2), as in /root/reference/proj/tools/erato.cpp:21-33.
+ *  - Table layout (driver.hpp:6-8): bit j of the table is bit (j mod 8) of
+ *    byte floor(j/8); 1 = 2(f*2^l+j)+1 is composite, 0 = prime.
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point fails with ERATO_GPU_E_NO_DEVICE.
+ */
+#ifndef ERATO_GPU_H
+#define ERATO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errc ordinals + 1 (params.hpp:18-29) */
+enum {
+  ERATO_GPU_OK = 0,
+  ERATO_GPU_L_OUT_OF_RANGE = 1,
+  ERATO_GPU_F_ZERO_OR_OVERLAP = 2,
+  ERATO_GPU_N_OUT_OF_RANGE = 3,
+  ERATO_GPU_OVERFLOW = 4,
+  ERATO_GPU_INDEX_OUT_OF_RANGE = 5,
+  ERATO_GPU_NOT_ADMISSIBLE = 6,
+  ERATO_GPU_ALLOC_LIMIT = 7,
+  ERATO_GPU_LIMIT_TOO_LARGE = 8,
+  ERATO_GPU_RANGE_TOO_LARGE = 9,
+  ERATO_GPU_IO_ERROR = 10,
+  /* GPU-side runtime errors (no reference counterpart; CLI exit 2) */
+  ERATO_GPU_E_CUDA = 64,
+  ERATO_GPU_E_NO_DEVICE = 65,
+  ERATO_GPU_E_INVALID_ARG = 66,
+};
+
+/* flags */
+#define ERATO_GPU_TEST_MODE 0x1u     /* l >= 4 instead of 10 (params.hpp:58-60) */
+#define ERATO_GPU_ALLOW_OVERLAP 0x2u /* accept u^2 <= v incl. f = 0 (SURVEY §8c convention:
+                                        multiples from max(u, p^2); 1 and primes stay 0) */
+
+/* RunStats (driver.hpp:24-32).  Times are seconds of device time (CUDA
+ * events); small_s covers masks+medium (tile kernel), large_s the bucket
+ * scatter, output_s the D2H / file part of the call. */
+typedef struct {
+  uint64_t prime_count; /* zero bits over the run */
+  uint64_t segments;    /* n */
+  double init_s;
+  double small_s;
+  double large_s;
+  double output_s;
+  double total_s;
+  uint64_t base_primes; /* odd primes <= isqrt(v) */
+  uint64_t tiles;       /* GPU tiles (2^log_tile bits each) */
+  uint32_t log_tile;
+  uint32_t waves;
+  uint32_t kernel_launches;
+  uint32_t retries; /* capacity re-runs after a bucket overflow */
+} erato_gpu_stats;
+
+/* ---- host-side parameter logic (no device needed) ---------------------- */
+
+/* validate_params (src/params.cpp:23-44); u/v may be NULL. */
+int erato_gpu_validate(unsigned l, uint64_t f, uint64_t n, unsigned flags, uint64_t* u,
+                       uint64_t* v);
+/* params_from_midpoint (src/params.cpp:64-77), decimal 10^e. */
+int erato_gpu_f_from_midpoint(unsigned e, unsigned l, uint64_t n, unsigned flags, uint64_t* f);
+/* isqrt (src/params.cpp:79-85). */
+uint64_t erato_gpu_isqrt(uint64_t x);
+/* first_offset, Lemma 1 (src/wheel.cpp:43-47). */
+uint32_t erato_gpu_first_offset(uint32_t p, unsigned l, uint64_t f);
+/* table_filename (src/driver.cpp:17-20); returns bytes needed incl. NUL. */
+size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, size_t cap);
+/* errc_name (src/params.cpp:7-21) for codes 1..10, plus the GPU codes. */
+const char* erato_gpu_errc_name(int code);
+/* Message of the last failure on this thread. */
+const char* erato_gpu_last_error(void);
+
+/* ---- device context ----------------------------------------------------- */
+/* Owns the device buffers, stream and cached tables for one CUDA device, so
+ * repeated runs (bench) reuse allocations.  Not thread-safe; one context per
+ * host thread / device.  device < 0 = current device. */
+typedef struct erato_gpu_ctx erato_gpu_ctx;
+int erato_gpu_create(int device, erato_gpu_ctx** out);
+void erato_gpu_destroy(erato_gpu_ctx* ctx);
+/* Number of CUDA devices visible (0 when none). */
+int erato_gpu_device_count(void);
+
+/* ---- the hot path: run_sieve (src/driver.cpp:83-120) --------------------- */
+
+/* Sieve (l, f, n) on the context's device.
+ *   dev_table  device pointer receiving n*2^(l-3) bytes (NULL = count only,
+ *              the NullSink path of bench.cpp:11-16);
+ *   dev_count  optional device pointer (uint64) receiving the zero-bit count
+ *              (lets a caller all-reduce it without a host round trip);
+ *   stream     cudaStream_t as void* (NULL = the context's stream);
+ *   sync       0: enqueue only, results valid after the stream drains
+ *              (stats->prime_count is then NOT filled); 1: wait and fill.
+ * The interval may be a shard of a larger run; see erato_gpu_shard. */
+int erato_gpu_run(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                  void* dev_table, uint64_t* dev_count, void* stream, int sync,
+                  erato_gpu_stats* stats);
+
+/* TableSink equivalent (driver.hpp:72-80): the whole table into host memory
+ * dst (dst_cap >= n*2^(l-3) bytes). */
+int erato_gpu_sieve_to_host(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n,
+                            unsigned flags, uint8_t* dst, size_t dst_cap, erato_gpu_stats* stats);
+
+/* NullSink run (count only): bench_run's timed_run (src/bench.cpp:11-16). */
+int erato_gpu_count(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                    uint64_t* count, erato_gpu_stats* stats);
+
+/* FileSink / write_table (driver.hpp:45-58, :98-99): writes
+ * out_dir/erato_l{l}_f{f}_n{n}.bits (exactly n*2^(l-3) bytes) and returns
+ * the path.  When (part_f, part_n) is a sub-range of (l, f, n) — one shard of
+ * a multi-GPU run — only that shard's bytes are pwrite()n at their offset
+ * into the shared file; pass part_n = 0 for the whole range. */
+int erato_gpu_write_table(erato_gpu_ctx* ctx, const char* out_dir, unsigned l, uint64_t f,
+                          uint64_t n, uint64_t part_f, uint64_t part_n, unsigned flags,
+                          char* path_out, size_t path_cap, erato_gpu_stats* stats);
+
+/* Contiguous range shard of (f, n) for rank `rank` of `world`:
+ * rank g gets segments [f + floor(g*n/world), f + floor((g+1)*n/world)). */
+void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_out,
+                     uint64_t* n_out);
+
+/* Ascending primes represented by the clear bits of an interval
+ * (extract_primes, src/driver.cpp:65-81), computed on the device.
+ * Writes up to cap primes to host dst; returns the count in *count. */
+int erato_gpu_extract_primes(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n,
+                             unsigned flags, uint64_t* dst, uint64_t cap, uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ERATO_GPU_H */

@@ -1,0 +1,655 @@
+// erato_gpu.cu — host orchestration + C ABI (include/erato_gpu.h).
+//
+// Replaces run_sieve (/root/reference/proj/src/driver.cpp:83-120) and its
+// sinks.  Per run:
+//   init  (base.cpp:19-89 analog, all on the device)
+//     1. odd primes < 2^16 (cached per context), Barrett constants
+//     2. sieve [1, isqrt(v)] with the tile kernel -> bitmap -> sorted u32
+//        prime list (popcount + scan compaction)
+//     3. one host sync: prime count and the class boundaries
+//     4. large primes: first hits (64-bit, __umul64hi) -> ML array + far
+//        wave buckets
+//   waves (the reference's per-segment loop, driver.cpp:93-117)
+//     for each wave of W tiles: scatter (large primes -> per-tile hit
+//     records, re-bucket) then tile kernel (patterns, medium, hits,
+//     popcount, 128-bit write-out)
+//   count: device u64 (NullSink: only it leaves the device).
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/erato_gpu.h"
+#include "sieve_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = std::string(erato_gpu_errc_name(code)) + ": " + msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(ERATO_GPU_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+uint64_t isqrt_u64(uint64_t x) {
+  uint64_t r = (uint64_t)std::sqrt((double)x);
+  if (r > UINT32_MAX) r = UINT32_MAX;
+  while (r > 0 && (unsigned __int128)r * r > x) --r;
+  while ((unsigned __int128)(r + 1) * (r + 1) <= x) ++r;
+  return r;
+}
+
+// Rosser–Schoenfeld: pi(x) < 1.25506 x / ln x for x > 1
+uint64_t pi_upper(uint64_t x) {
+  if (x < 17) return 8;
+  return (uint64_t)(1.25506 * (double)x / std::log((double)x)) + 16;
+}
+
+constexpr uint32_t kBaseLogTile = 20;  // tile size for the sieve of [1, sqrt(v)]
+
+}  // namespace
+
+struct erato_gpu_ctx {
+  int device = 0;
+  int nsm = 0;
+  cudaStream_t stream = nullptr;
+  // cached per context
+  DevBuf sp, spm, ptab;  // small primes < 2^16, their Barrett constants, pattern tables
+  std::vector<uint32_t> h_sp;
+  // grow-only run buffers
+  DevBuf base_bits, primes, mm, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
+  double hcap_scale = 1.0, bcap_scale = 1.0;
+  cudaEvent_t ev[4] = {};
+};
+
+extern "C" {
+
+const char* erato_gpu_errc_name(int code) {
+  switch (code) {
+    case ERATO_GPU_OK: return "OK";
+    case ERATO_GPU_L_OUT_OF_RANGE: return "L_OUT_OF_RANGE";
+    case ERATO_GPU_F_ZERO_OR_OVERLAP: return "F_ZERO_OR_OVERLAP";
+    case ERATO_GPU_N_OUT_OF_RANGE: return "N_OUT_OF_RANGE";
+    case ERATO_GPU_OVERFLOW: return "OVERFLOW";
+    case ERATO_GPU_INDEX_OUT_OF_RANGE: return "INDEX_OUT_OF_RANGE";
+    case ERATO_GPU_NOT_ADMISSIBLE: return "NOT_ADMISSIBLE";
+    case ERATO_GPU_ALLOC_LIMIT: return "ALLOC_LIMIT";
+    case ERATO_GPU_LIMIT_TOO_LARGE: return "LIMIT_TOO_LARGE";
+    case ERATO_GPU_RANGE_TOO_LARGE: return "RANGE_TOO_LARGE";
+    case ERATO_GPU_IO_ERROR: return "IO_ERROR";
+    case ERATO_GPU_E_CUDA: return "CUDA_ERROR";
+    case ERATO_GPU_E_NO_DEVICE: return "NO_DEVICE";
+    case ERATO_GPU_E_INVALID_ARG: return "INVALID_ARGUMENT";
+  }
+  return "UNKNOWN";
+}
+
+const char* erato_gpu_last_error(void) { return g_err.c_str(); }
+
+uint64_t erato_gpu_isqrt(uint64_t x) { return isqrt_u64(x); }
+
+// validate_params, /root/reference/proj/src/params.cpp:23-44
+int erato_gpu_validate(unsigned l, uint64_t f, uint64_t n, unsigned flags, uint64_t* u, uint64_t* v) {
+  const unsigned lmin = (flags & ERATO_GPU_TEST_MODE) ? 4 : 10;
+  if (l < lmin || l > 30)
+    return fail(ERATO_GPU_L_OUT_OF_RANGE,
+                "l=" + std::to_string(l) + " outside [" + std::to_string(lmin) + ", 30]");
+  if (n == 0) return fail(ERATO_GPU_N_OUT_OF_RANGE, "n must be >= 1");
+  if (f > UINT64_MAX - n || (f + n) > (UINT64_MAX >> (l + 1)))
+    return fail(ERATO_GPU_OVERFLOW, "v = (f+n)*2^(l+1) exceeds 2^64");
+  const uint64_t uu = (f << (l + 1)) + 1, vv = (f + n) << (l + 1);
+  if (!(flags & ERATO_GPU_ALLOW_OVERLAP) && (unsigned __int128)uu * uu <= vv)
+    return fail(ERATO_GPU_F_ZERO_OR_OVERLAP,
+                "interval overlaps its own base primes (need u^2 > v); f=" + std::to_string(f));
+  if (u) *u = uu;
+  if (v) *v = vv;
+  return 0;
+}
+
+// params_from_midpoint, /root/reference/proj/src/params.cpp:64-77
+int erato_gpu_f_from_midpoint(unsigned e, unsigned l, uint64_t n, unsigned flags, uint64_t* f) {
+  if (e > 19) return fail(ERATO_GPU_OVERFLOW, "10^" + std::to_string(e) + " exceeds 2^64");
+  uint64_t pow10 = 1;
+  for (unsigned i = 0; i < e; ++i) pow10 *= 10;
+  if (l > 30) return fail(ERATO_GPU_L_OUT_OF_RANGE, "l=" + std::to_string(l));
+  const uint64_t mid = pow10 >> (l + 1);
+  if (mid <= n / 2)
+    return fail(ERATO_GPU_F_ZERO_OR_OVERLAP,
+                "midpoint 10^" + std::to_string(e) + " below half the interval");
+  const uint64_t ff = mid - n / 2;
+  const int rc = erato_gpu_validate(l, ff, n, flags & ERATO_GPU_TEST_MODE, nullptr, nullptr);
+  if (rc) return rc;
+  *f = ff;
+  return 0;
+}
+
+// first_offset, /root/reference/proj/src/wheel.cpp:43-47
+uint32_t erato_gpu_first_offset(uint32_t p, unsigned l, uint64_t f) {
+  const uint64_t r = ((f % p) << (l + 1)) % p;
+  return (uint32_t)(r % 2 == 0 ? (p - r - 1) / 2 : (2 * (uint64_t)p - r - 1) / 2);
+}
+
+// table_filename, /root/reference/proj/src/driver.cpp:17-20
+size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, size_t cap) {
+  const std::string s = "erato_l" + std::to_string(l) + "_f" + std::to_string(f) + "_n" +
+                        std::to_string(n) + ".bits";
+  if (out && cap) std::snprintf(out, cap, "%s", s.c_str());
+  return s.size() + 1;
+}
+
+void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_out, uint64_t* n_out) {
+  if (world < 1) world = 1;
+  const unsigned __int128 b = (unsigned __int128)n * (unsigned)rank / (unsigned)world;
+  const unsigned __int128 e = (unsigned __int128)n * (unsigned)(rank + 1) / (unsigned)world;
+  *f_out = f + (uint64_t)b;
+  *n_out = (uint64_t)(e - b);
+}
+
+int erato_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int erato_gpu_create(int device, erato_gpu_ctx** out) {
+  if (!out) return fail(ERATO_GPU_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (erato_gpu_device_count() == 0) return fail(ERATO_GPU_E_NO_DEVICE, "no CUDA device visible");
+  if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new erato_gpu_ctx();
+  c->device = device;
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  c->nsm = prop.multiProcessorCount;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8)));
+  // cached tables: small primes < 2^16 and the pattern windows
+  CUDA_TRY(c->sp.ensure(8192 * 4));
+  CUDA_TRY(c->spm.ensure(8192 * 8));
+  CUDA_TRY(c->ptab.ensure(eg::kPatWords * 4));
+  CUDA_TRY(c->scal.ensure(64 * 8));
+  eg::k_build_patterns<<<(eg::kPatWords + 255) / 256, 256, 0, c->stream>>>(c->ptab.as<uint32_t>());
+  eg::k_small_primes<<<1, 1024, 0, c->stream>>>(c->sp.as<uint32_t>(), c->scal.as<uint32_t>());
+  uint32_t nsp = 0;
+  CUDA_TRY(cudaMemcpyAsync(&nsp, c->scal.p, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  eg::k_barrett<<<(nsp + 255) / 256, 256, 0, c->stream>>>(c->sp.as<uint32_t>(), c->spm.as<uint64_t>(), nsp);
+  c->h_sp.resize(nsp);
+  CUDA_TRY(cudaMemcpyAsync(c->h_sp.data(), c->sp.p, nsp * 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaGetLastError());
+  *out = c;
+  return 0;
+}
+
+void erato_gpu_destroy(erato_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->mm, &c->ml, &c->buckets,
+                    &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
+                    &c->outbuf})
+    b->release();
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Launch the tile kernel over `ntiles` tiles starting at `tile0`.
+void launch_tiles(erato_gpu_ctx* c, cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles) {
+  const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8;
+  eg::k_tile<<<ntiles, eg::kTileThreads, smem, st>>>(a);
+}
+
+// Sorted list of the zero bits of bits[0..nbits) at indices >= lo, as base + 2*j.
+template <class T>
+int compact_zeros(erato_gpu_ctx* c, cudaStream_t st, const uint32_t* bits, uint64_t nbits, uint64_t lo,
+                  uint64_t base, T* out, uint64_t cap, uint64_t* d_total) {
+  const uint64_t nwords = (nbits + 31) / 32;
+  const uint64_t nblk = (nwords + eg::kCompactWords - 1) / eg::kCompactWords;
+  if (nblk == 0) {
+    CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, st));
+    return 0;
+  }
+  if (nblk > (1u << 26)) return fail(ERATO_GPU_RANGE_TOO_LARGE, "compaction too large");
+  CUDA_TRY(c->blk_cnt.ensure(nblk * 4));
+  CUDA_TRY(c->blk_off.ensure(nblk * 8));
+  eg::k_count_zeros_blocks<<<(unsigned)nblk, 1024, 0, st>>>(bits, nbits, lo, c->blk_cnt.as<uint32_t>());
+  eg::k_scan_counts<<<1, 1024, 0, st>>>(c->blk_cnt.as<uint32_t>(), (uint32_t)nblk, c->blk_off.as<uint64_t>(),
+                                        d_total);
+  eg::k_write_zeros<T><<<(unsigned)nblk, 1024, 0, st>>>(bits, nbits, lo, c->blk_off.as<uint64_t>(), base, out,
+                                                        cap);
+  return 0;
+}
+
+struct Plan {
+  unsigned l;
+  uint64_t f, n, u, v, T, g0;
+  uint32_t log_s, S, W, WS;
+  uint64_t ntiles, nwaves;
+  bool overlap;
+};
+
+}  // namespace
+
+extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                             void* dev_table, uint64_t* dev_count, void* stream_v, int sync,
+                             erato_gpu_stats* stats) {
+  if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
+  Plan P{};
+  int rc = erato_gpu_validate(l, f, n, flags, &P.u, &P.v);
+  if (rc) return rc;
+  if (dev_table && ((uintptr_t)dev_table & 15))
+    return fail(ERATO_GPU_E_INVALID_ARG, "dev_table must be 16-byte aligned");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = stream_v ? (cudaStream_t)stream_v : c->stream;
+  P.l = l;
+  P.f = f;
+  P.n = n;
+  P.T = n << l;
+  P.g0 = f << l;
+  P.overlap = (unsigned __int128)P.u * P.u <= P.v;
+  // tile size: 2^20 bits unless the run is too small to fill the GPU
+  {
+    uint32_t ls = 20;
+    while (ls > 13 && (P.T >> ls) < (uint64_t)2 * c->nsm) --ls;
+    P.log_s = ls;
+    P.S = 1u << ls;
+  }
+  P.ntiles = (P.T + P.S - 1) >> P.log_s;
+  {
+    int occ = 1;
+    const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile, eg::kTileThreads, smem));
+    if (occ < 1) occ = 1;
+    uint64_t W = (uint64_t)c->nsm * occ;
+    W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
+    W = std::min<uint64_t>(W, ((uint64_t)1 << 29) / P.S);  // WS <= 2^29 (entry encoding)
+    W = std::min<uint64_t>(W, P.ntiles);
+    P.W = (uint32_t)std::max<uint64_t>(W, 1);
+  }
+  P.WS = P.W * P.S;
+  P.nwaves = (P.ntiles + P.W - 1) / P.W;
+
+  uint32_t launches = 0;
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t vroot = isqrt_u64(P.v);
+    CUDA_TRY(cudaEventRecord(c->ev[0], st));
+    // ---------------- 1-2. base primes <= sqrt(v) ----------------
+    uint64_t nbase_bits = (vroot + 1) / 2;  // odd numbers 1..vroot
+    const uint64_t prime_cap = pi_upper(vroot) + 64;
+    CUDA_TRY(c->primes.ensure(prime_cap * 4));
+    uint64_t* d_scal = c->scal.as<uint64_t>();  // [0] total primes, [8..] bounds, [16] count, [17] overflow
+    if (nbase_bits > 1) {
+      const uint64_t words = ((nbase_bits + ((1u << kBaseLogTile) - 1)) >> kBaseLogTile) << (kBaseLogTile - 5);
+      CUDA_TRY(c->base_bits.ensure(words * 4));
+      const uint64_t rr = isqrt_u64(vroot);
+      // small primes in (61, rr]
+      const auto b61 = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), 61u) - c->h_sp.begin();
+      const auto brr = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), (uint32_t)std::min<uint64_t>(rr, 65535)) -
+                       c->h_sp.begin();
+      eg::TileArgs ta{};
+      ta.g0 = 0;
+      ta.tbits = nbase_bits;
+      ta.tile0 = 0;
+      ta.log_s = kBaseLogTile;
+      ta.mp = c->sp.as<uint32_t>() + b61;
+      ta.mm = c->spm.as<uint64_t>() + b61;
+      ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
+      {
+        const auto bw = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), (1u << kBaseLogTile) / 64) - c->h_sp.begin();
+        ta.nmed_warp = (uint32_t)std::min<int64_t>(std::max<int64_t>(bw - b61, 0), ta.nmed);
+      }
+      ta.ptab = c->ptab.as<uint32_t>();
+      ta.table = c->base_bits.as<uint32_t>();
+      ta.count = reinterpret_cast<unsigned long long*>(d_scal + 20);
+      ta.p2_floor = 1;
+      const uint64_t bt = (nbase_bits + (1u << kBaseLogTile) - 1) >> kBaseLogTile;
+      launch_tiles(c, st, ta, (uint32_t)bt);
+      ++launches;
+      rc = compact_zeros<uint32_t>(c, st, c->base_bits.as<uint32_t>(), nbase_bits, 1, 1, c->primes.as<uint32_t>(),
+                                   prime_cap, d_scal + 0);
+      if (rc) return rc;
+      launches += 3;
+    } else {
+      CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
+    }
+    // ---------------- 3. class boundaries (one host sync) ----------------
+    uint64_t thr[4] = {61, (uint64_t)P.S / 64, P.S, P.WS};
+    CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
+    eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 4, d_scal + 8);
+    ++launches;
+    uint64_t hb[12];
+    CUDA_TRY(cudaMemcpyAsync(hb, d_scal, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const uint64_t nprimes = hb[0];
+    const uint64_t i61 = hb[8], iwarp = std::max(hb[9], hb[8]), iS = hb[10], iWS = hb[11];
+    if (nprimes > (uint64_t{1} << 27))
+      return fail(ERATO_GPU_ALLOC_LIMIT, std::to_string(nprimes) + " base primes exceed cap 134217728");
+    uint32_t pmax = 0;
+    if (nprimes) CUDA_TRY(cudaMemcpy(&pmax, c->primes.as<uint32_t>() + nprimes - 1, 4, cudaMemcpyDeviceToHost));
+
+    // ---------------- 4. medium constants + large-prime structures ----------------
+    const uint64_t nmed = iS - i61, nml = iWS - iS, nfar = nprimes - iWS;
+    CUDA_TRY(c->mm.ensure(std::max<uint64_t>(nmed, 1) * 8));
+    if (nmed)
+      eg::k_barrett<<<(unsigned)((nmed + 255) / 256), 256, 0, st>>>(c->primes.as<uint32_t>() + i61, c->mm.as<uint64_t>(),
+                                                                     (uint32_t)nmed);
+    ++launches;
+    const bool have_large = nml + nfar > 0;
+    uint32_t ring = 1, bcap = 1, hcap = 4;
+    if (have_large) {
+      const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
+      const double sum_recip = std::max(0.0, std::log(lnP / std::log((double)P.S))) + 0.02;  // sum 1/p, S<p<=P
+      double eh = (double)P.S * (8.0 / 15.0) * sum_recip;
+      hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
+      hcap = (hcap + 3) & ~3u;
+      CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
+      CUDA_TRY(c->hits.ensure((uint64_t)P.W * hcap * 4));
+      CUDA_TRY(c->hitcnt.ensure((uint64_t)P.W * 4));
+      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
+      if (nfar) {
+        ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.WS + 3, P.nwaves + 2);
+        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.WS))) + 0.01;
+        const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
+        bcap = (uint32_t)std::min<double>((eb * 1.10 + 8192) * c->bcap_scale, (double)nfar + 64);
+      }
+      CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 8));
+      CUDA_TRY(c->bcount.ensure((uint64_t)ring * 4 + 4));
+      CUDA_TRY(cudaMemsetAsync(c->bcount.p, 0, (uint64_t)ring * 4 + 4, st));
+      CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));  // overflow flag
+      eg::SetupArgs sa{};
+      sa.primes = c->primes.as<uint32_t>();
+      sa.i0 = iS;
+      sa.i_ml_end = iWS;
+      sa.i_end = nprimes;
+      sa.x0 = 2 * P.g0 + 1;
+      sa.ml = c->ml.as<uint64_t>();
+      sa.buckets = c->buckets.as<uint64_t>();
+      sa.bcount = c->bcount.as<uint32_t>();
+      sa.ring = ring;
+      sa.bcap = bcap;
+      sa.nwaves = P.nwaves;
+      sa.WS = P.WS;
+      sa.inv_ws = 1.0 / (double)P.WS;
+      sa.overflow = reinterpret_cast<int*>(d_scal + 17);
+      const uint64_t nl = nprimes - iS;
+      eg::k_setup_large<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(sa);
+      ++launches;
+    } else {
+      CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[1], st));
+
+    // ---------------- 5. waves ----------------
+    unsigned long long* d_count = reinterpret_cast<unsigned long long*>(d_scal + 16);
+    CUDA_TRY(cudaMemsetAsync(d_count, 0, 8, st));
+    eg::TileArgs ta{};
+    ta.g0 = P.g0;
+    ta.tbits = P.T;
+    ta.log_s = P.log_s;
+    ta.mp = c->primes.as<uint32_t>() + i61;
+    ta.mm = c->mm.as<uint64_t>();
+    ta.nmed = (uint32_t)nmed;
+    ta.nmed_warp = (uint32_t)std::min<uint64_t>(iwarp - i61, nmed);
+    ta.ptab = c->ptab.as<uint32_t>();
+    ta.hits = have_large ? c->hits.as<uint32_t>() : nullptr;
+    ta.hitcnt = c->hitcnt.as<uint32_t>();
+    ta.hcap = hcap;
+    ta.table = static_cast<uint32_t*>(dev_table);
+    ta.count = d_count;
+    ta.p2_floor = P.overlap ? 1 : 0;
+    eg::ScatterArgs sc{};
+    if (have_large) {
+      sc.ml = c->ml.as<uint64_t>();
+      sc.nml = (uint32_t)nml;
+      sc.ml_blocks = nml ? (uint32_t)std::min<uint64_t>((nml + eg::kScatterThreads * eg::kMlEPT - 1) /
+                                                            (eg::kScatterThreads * eg::kMlEPT),
+                                                        (uint64_t)c->nsm * 4)
+                         : 0;
+      sc.buckets = c->buckets.as<uint64_t>();
+      sc.bcount = c->bcount.as<uint32_t>();
+      sc.ring = ring;
+      sc.bcap = bcap;
+      sc.nwaves = P.nwaves;
+      sc.log_s = P.log_s;
+      sc.WS = P.WS;
+      sc.inv_ws = 1.0 / (double)P.WS;
+      sc.hits = c->hits.as<uint32_t>();
+      sc.hitcnt = c->hitcnt.as<uint32_t>();
+      sc.hcap = hcap;
+      sc.overflow = reinterpret_cast<int*>(d_scal + 17);
+    }
+    const uint32_t far_blocks = nfar ? (uint32_t)c->nsm * 2 : 0;
+    for (uint64_t w = 0; w < P.nwaves; ++w) {
+      const uint64_t tile0 = w * P.W;
+      const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
+      if (have_large) {
+        sc.wave = w;
+        sc.ntiles_w = ntw;
+        const uint32_t slot = nfar ? (uint32_t)(w % ring) : 0;
+        sc.far_in = c->buckets.as<uint64_t>() + (uint64_t)slot * bcap;
+        sc.far_in_count = c->bcount.as<uint32_t>() + slot;
+        eg::k_scatter<<<sc.ml_blocks + far_blocks, eg::kScatterThreads, 0, st>>>(sc);
+        ++launches;
+        ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
+      }
+      ta.tile0 = tile0;
+      launch_tiles(c, st, ta, ntw);
+      ++launches;
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (dev_count) CUDA_TRY(cudaMemcpyAsync(dev_count, d_count, 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaEventRecord(c->ev[2], st));
+    if (!sync) {
+      if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->segments = n;
+        stats->base_primes = nprimes;
+        stats->tiles = P.ntiles;
+        stats->log_tile = P.log_s;
+        stats->waves = (uint32_t)P.nwaves;
+        stats->kernel_launches = launches;
+      }
+      return 0;  // overflow cannot be checked without a sync; capacities are generous
+    }
+    uint64_t res[2];
+    CUDA_TRY(cudaMemcpyAsync(res, d_scal + 16, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if ((int)res[1] != 0) {
+      if (attempt >= 4) return fail(ERATO_GPU_ALLOC_LIMIT, "bucket capacity overflow persists");
+      c->hcap_scale *= 2.0;
+      c->bcap_scale *= 2.0;
+      if (stats) stats->retries = attempt + 1;
+      continue;
+    }
+    if (stats) {
+      float t_init = 0, t_tot = 0;
+      cudaEventElapsedTime(&t_init, c->ev[0], c->ev[1]);
+      cudaEventElapsedTime(&t_tot, c->ev[0], c->ev[2]);
+      const uint32_t retries = stats->retries;
+      std::memset(stats, 0, sizeof(*stats));
+      stats->retries = retries;
+      stats->prime_count = res[0];
+      stats->segments = n;
+      stats->init_s = t_init * 1e-3;
+      stats->small_s = (t_tot - t_init) * 1e-3;
+      stats->total_s = t_tot * 1e-3;
+      stats->base_primes = nprimes;
+      stats->tiles = P.ntiles;
+      stats->log_tile = P.log_s;
+      stats->waves = (uint32_t)P.nwaves;
+      stats->kernel_launches = launches;
+    }
+    return 0;
+  }
+}
+
+extern "C" int erato_gpu_count(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                               uint64_t* count, erato_gpu_stats* stats) {
+  erato_gpu_stats local{};
+  erato_gpu_stats* s = stats ? stats : &local;
+  std::memset(s, 0, sizeof(*s));
+  const int rc = erato_gpu_run(c, l, f, n, flags, nullptr, nullptr, nullptr, 1, s);
+  if (rc) return rc;
+  if (count) *count = s->prime_count;
+  return 0;
+}
+
+extern "C" int erato_gpu_sieve_to_host(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                                       uint8_t* dst, size_t dst_cap, erato_gpu_stats* stats) {
+  if (!c || !dst) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
+  int rc = erato_gpu_validate(l, f, n, flags, nullptr, nullptr);
+  if (rc) return rc;
+  const uint64_t bytes = (n << l) / 8;
+  if (dst_cap < bytes) return fail(ERATO_GPU_E_INVALID_ARG, "dst_cap < table bytes");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->table.ensure((bytes + 15) & ~15ull));
+  erato_gpu_stats local{};
+  erato_gpu_stats* s = stats ? stats : &local;
+  std::memset(s, 0, sizeof(*s));
+  rc = erato_gpu_run(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, s);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dst, c->table.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]);
+  s->output_s = ms * 1e-3;
+  return 0;
+}
+
+extern "C" int erato_gpu_write_table(erato_gpu_ctx* c, const char* out_dir, unsigned l, uint64_t f, uint64_t n,
+                                     uint64_t part_f, uint64_t part_n, unsigned flags, char* path_out,
+                                     size_t path_cap, erato_gpu_stats* stats) {
+  if (!c || !out_dir) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
+  int rc = erato_gpu_validate(l, f, n, flags, nullptr, nullptr);
+  if (rc) return rc;
+  if (part_n == 0) {
+    part_f = f;
+    part_n = n;
+  }
+  if (part_f < f || part_f + part_n > f + n) return fail(ERATO_GPU_E_INVALID_ARG, "part outside (f, n)");
+  // FileSink: create_directories + exact name (driver.cpp:29-36)
+  std::string dir(out_dir);
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0777);
+  char name[128];
+  erato_gpu_table_filename(l, f, n, name, sizeof(name));
+  const std::string path = dir + (dir.empty() || dir.back() == '/' ? "" : "/") + name;
+  const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT, 0644);
+  if (fd < 0) return fail(ERATO_GPU_IO_ERROR, "cannot open " + path);
+  const uint64_t total_bytes = (n << l) / 8;
+  if (part_f == f && part_n == n) {
+    if (::ftruncate(fd, (off_t)total_bytes) != 0) {
+      ::close(fd);
+      return fail(ERATO_GPU_IO_ERROR, "truncate failed for " + path);
+    }
+  }
+  const uint64_t bytes = (part_n << l) / 8;
+  const uint64_t off = ((part_f - f) << l) / 8;
+  std::vector<uint8_t> host;
+  uint8_t* pinned = nullptr;
+  if (cudaMallocHost(&pinned, bytes ? bytes : 1) != cudaSuccess) {
+    cudaGetLastError();
+    pinned = nullptr;
+    host.resize(bytes);
+  }
+  uint8_t* dst = pinned ? pinned : host.data();
+  rc = erato_gpu_sieve_to_host(c, l, part_f, part_n, flags, dst, bytes, stats);
+  if (rc) {
+    if (pinned) cudaFreeHost(pinned);
+    ::close(fd);
+    return rc;
+  }
+  uint64_t done = 0;
+  while (done < bytes) {
+    const ssize_t w = ::pwrite(fd, dst + done, (size_t)std::min<uint64_t>(bytes - done, 1ull << 30), (off_t)(off + done));
+    if (w <= 0) {
+      if (pinned) cudaFreeHost(pinned);
+      ::close(fd);
+      return fail(ERATO_GPU_IO_ERROR, "short write to " + path);
+    }
+    done += (uint64_t)w;
+  }
+  if (pinned) cudaFreeHost(pinned);
+  if (::close(fd) != 0) return fail(ERATO_GPU_IO_ERROR, "close failed for " + path);
+  if (path_out && path_cap) std::snprintf(path_out, path_cap, "%s", path.c_str());
+  return 0;
+}
+
+extern "C" int erato_gpu_extract_primes(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                                        uint64_t* dst, uint64_t cap, uint64_t* count) {
+  if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
+  uint64_t u = 0, v = 0;
+  int rc = erato_gpu_validate(l, f, n, flags, &u, &v);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint64_t T = n << l;
+  CUDA_TRY(c->table.ensure(((T / 8) + 15) & ~15ull));
+  erato_gpu_stats s{};
+  rc = erato_gpu_run(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, &s);
+  if (rc) return rc;
+  // the number 1 (bit 0 of an f = 0 run) is a clear bit but not a prime
+  const uint64_t lo = (u == 1) ? 1 : 0;
+  const uint64_t np = s.prime_count - lo;
+  CUDA_TRY(c->outbuf.ensure(std::max<uint64_t>(np, 1) * 8));
+  uint64_t* d_total = c->scal.as<uint64_t>() + 40;
+  // extract_primes (driver.cpp:65-81): clear bits -> u + 2j
+  rc = compact_zeros<uint64_t>(c, c->stream, c->table.as<uint32_t>(), T, lo, u, c->outbuf.as<uint64_t>(), np, d_total);
+  if (rc) return rc;
+  const uint64_t m = std::min(np, cap);
+  if (dst && m) CUDA_TRY(cudaMemcpyAsync(dst, c->outbuf.p, m * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (count) *count = np;
+  return 0;
+}

@@ -1,0 +1,662 @@
+// sieve_kernels.cuh — sm_100a device code of the segmented odd-only sieve.
+//
+// Geometry (reference: /root/reference/proj/include/erato/params.hpp:1-9):
+// global odd index i stands for the number 2i+1; table bit j of a run
+// (l, f, n) is global index f*2^l + j.  The GPU does not process the
+// reference's 2^l-bit segments one after another; it processes TILES of
+// S = 2^log_s bits (S is decoupled from l — the output is position
+// independent), many tiles at once, one CTA per tile, with
+// the tile resident in shared memory.
+//
+// Prime classes (GPU split; the reference's split is base.cpp:11-17):
+//   small   p <= 61        periodic word patterns (masks.cpp:9-50 idea)
+//   medium  61 < p <= S    shared-memory atomicOr marking inside the tile,
+//                          start offset recomputed per tile (64-bit Barrett,
+//                          __umul64hi), mod-30 wheel over the cofactor
+//                          (wheel.cpp:10-69 idea: 8 of 15 odd cofactors)
+//   large   p > S          bucketed: (p,q) entries scattered into the wave
+//                          of their next hit, which emits per-tile hit
+//                          records; the paper's circle/bucket idea
+//                          (large_kernel.hpp, Lemma 2) rebuilt for
+//                          a machine that processes ~148 tiles at once.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace eg {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// mod-30 wheel over odd cofactors c of p*c.  Admissible residues (coprime to
+// 30): R = {1,7,11,13,17,19,23,29}; class s <-> R[s].  In index space the
+// step from class s to s+1 is D[s]*p with D = {3,2,1,2,1,2,3,1} — the
+// reference's wheel deltas (src/wheel.cpp:27-30).
+__device__ __forceinline__ uint32_t wheel_D(uint32_t s) { return (0x13212123u >> (s << 2)) & 15u; }
+
+// adv[r]: smallest a >= 0 with r+a admissible; cls[r]: class of admissible r.
+__constant__ uint8_t c_adv[30] = {1, 0, 5, 4, 3, 2, 1, 0, 3, 2, 1, 0, 1, 0, 3,
+                                  2, 1, 0, 1, 0, 3, 2, 1, 0, 5, 4, 3, 2, 1, 0};
+__constant__ uint8_t c_cls[30] = {255, 0,   255, 255, 255, 255, 255, 1,   255, 255,
+                                  255, 2,   255, 3,   255, 255, 255, 4,   255, 5,
+                                  255, 255, 255, 6,   255, 255, 255, 255, 255, 7};
+// cum[s][t] = sum_{i<t} D[(s+i)&7]
+__constant__ uint8_t c_cum[8][8] = {
+    {0, 3, 5, 6, 8, 9, 11, 14}, {0, 2, 3, 5, 6, 8, 11, 12}, {0, 1, 3, 4, 6, 9, 10, 13},
+    {0, 2, 3, 5, 8, 9, 12, 14}, {0, 1, 3, 6, 7, 10, 12, 13}, {0, 2, 5, 6, 9, 11, 12, 14},
+    {0, 3, 4, 7, 9, 10, 12, 13}, {0, 1, 4, 6, 7, 9, 10, 12}};
+
+__device__ __forceinline__ uint32_t mod30_u64(uint64_t c) {
+  const uint32_t hi = (uint32_t)(c >> 32), lo = (uint32_t)c;
+  return ((hi % 30u) * 16u + lo % 30u) % 30u;  // 2^32 = 16 (mod 30)
+}
+
+// First wheel-admissible multiple p*c >= x with c >= cmin, for odd x = 2g+1
+// (g = global odd index of the tile start).  Returns its index offset from g,
+// (c*p - x)/2, and the wheel class s of c.  minv = floor((2^64-1)/p).
+// Restates Lemma 1 / first_offset (src/wheel.cpp:43-47) plus wheel_align
+// (src/wheel.cpp:60-69) for 64-bit starts without a 128-bit remainder.
+__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t minv, uint64_t x, uint64_t cmin,
+                                              uint32_t& s) {
+  uint64_t c = __umul64hi(x, minv);  // floor(x/p) - {0,1,2}
+  uint64_t r = x - c * p;
+  while (r >= p) {
+    r -= p;
+    ++c;
+  }
+  uint64_t d = 0;  // c*p - x after rounding c up
+  if (r) {
+    ++c;
+    d = p - r;
+  }
+  if (c < cmin) {
+    d += (cmin - c) * (uint64_t)p;
+    c = cmin;
+  }
+  const uint32_t cm = mod30_u64(c);
+  const uint32_t a = c_adv[cm];
+  s = c_cls[cm + a];
+  d += (uint64_t)a * p;
+  return d >> 1;
+}
+
+// ---------------------------------------------------------------------------
+// Small-prime patterns.  Eight groups of primes 3..61 with product moduli M;
+// table entry c of group k is the 32-bit window of the group's composite
+// pattern starting at pattern phase 32c mod M (gcd(32, M) = 1, so one word
+// step = one entry step).  Bit b of entry c is set iff (32c+b) = (p-1)/2
+// (mod p) for a p of the group (masks.hpp:4-12).
+constexpr int kNumGroups = 8;
+constexpr uint32_t kPatWords = 10240;  // 10238 rounded to a multiple of 4
+__constant__ uint32_t c_gmod[kNumGroups] = {105, 143, 323, 667, 1147, 1763, 2491, 3599};
+__constant__ uint32_t c_goff[kNumGroups] = {0, 105, 248, 571, 1238, 2385, 4148, 6639};
+__constant__ uint32_t c_ginv32[kNumGroups] = {23, 76, 212, 271, 466, 1157, 1012, 1912};
+__constant__ uint8_t c_gprimes[kNumGroups][3] = {{3, 5, 7},   {11, 13, 0}, {17, 19, 0}, {23, 29, 0},
+                                                 {31, 37, 0}, {41, 43, 0}, {47, 53, 0}, {59, 61, 0}};
+__constant__ uint8_t c_small17[17] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61};
+
+__global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kPatWords) return;
+  int k = kNumGroups - 1;
+  while (k > 0 && i < c_goff[k]) --k;
+  const uint32_t M = c_gmod[k];
+  const uint32_t c = i - c_goff[k];
+  if (c >= M) {  // padding words
+    ptab[i] = 0;
+    return;
+  }
+  uint32_t w = 0;
+  for (uint32_t b = 0; b < 32; ++b) {
+    const uint32_t x = (32u * c + b) % M;
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t p = c_gprimes[k][j];
+      if (p && x % p == (p - 1) / 2) w |= 1u << b;
+    }
+  }
+  ptab[i] = w;
+}
+
+// ---------------------------------------------------------------------------
+// Tile kernel: one CTA = one S-bit tile in shared memory.
+struct TileArgs {
+  uint64_t g0;     // global odd index of table bit 0 (= f << l)
+  uint64_t tbits;  // table bits T of this run (shard)
+  uint64_t tile0;  // first tile of this launch
+  uint32_t log_s;
+  const uint32_t* mp;  // medium primes (61 < p <= S, <= sqrt(v)), ascending
+  const uint64_t* mm;  // floor((2^64-1)/p)
+  uint32_t nmed;
+  uint32_t nmed_warp;    // the first nmed_warp medium primes are marked warp-per-prime
+  const uint32_t* ptab;  // kPatWords pattern words (global)
+  const uint32_t* hits;  // [gridDim.x][hcap] hit offsets (large primes), may be null
+  uint32_t* hitcnt;      // [gridDim.x], zeroed after use
+  uint32_t hcap;
+  uint32_t* table;               // output words (nullable: count only)
+  unsigned long long* count;     // zero-bit accumulator
+  uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
+  int p2_floor;                  // 1: medium multiples from p^2 (overlap runs, base sieve)
+};
+
+constexpr int kTileThreads = 1024;
+
+__global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
+  extern __shared__ uint4 smem4[];
+  uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
+  uint32_t* const tile = pat + kPatWords;
+  __shared__ uint32_t s_item;
+  __shared__ unsigned long long s_red[kTileThreads / 32];
+
+  const uint32_t tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t log_s = a.log_s;
+  const uint32_t S = 1u << log_s, nw = S >> 5;
+  const uint64_t tstart = (a.tile0 + blockIdx.x) << log_s;
+  const uint64_t g = a.g0 + tstart;
+
+  {  // stage pattern tables
+    const uint4* src = reinterpret_cast<const uint4*>(a.ptab);
+    for (uint32_t i = tid; i < kPatWords / 4; i += bd) smem4[i] = src[i];
+  }
+  if (tid == 0) s_item = 0;
+  __syncthreads();
+
+  // 1. small primes: OR of the 8 group windows, plain stores
+  {
+    uint32_t cur[kNumGroups], stp[kNumGroups];
+#pragma unroll
+    for (int k = 0; k < kNumGroups; ++k) {
+      const uint32_t M = c_gmod[k];
+      const uint32_t cg = (uint32_t)((g % M) * c_ginv32[k] % M);
+      cur[k] = (cg + tid) % M;
+      stp[k] = bd % M;
+    }
+    for (uint32_t w = tid; w < nw; w += bd) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int k = 0; k < kNumGroups; ++k) {
+        v |= pat[c_goff[k] + cur[k]];
+        cur[k] += stp[k];
+        if (cur[k] >= c_gmod[k]) cur[k] -= c_gmod[k];
+      }
+      tile[w] = v;
+    }
+  }
+  __syncthreads();
+  // the patterns also hit the primes 3..61 themselves: clear them if inside
+  if (tid < 17) {
+    const uint64_t idx = (c_small17[tid] - 1) / 2;
+    if (idx >= g && idx < g + S) {
+      const uint32_t q = (uint32_t)(idx - g);
+      atomicAnd(&tile[q >> 5], ~(1u << (q & 31)));
+    }
+  }
+
+  // 2. medium primes, dynamic work list: warp-per-prime items first (most
+  // marks), then 32-primes-per-warp items.
+  {
+    const uint64_t x = 2 * g + 1;
+    const uint32_t nitem = a.nmed_warp + (a.nmed - a.nmed_warp + 31) / 32;
+    for (;;) {
+      uint32_t item = 0;
+      if (lane == 0) item = atomicAdd(&s_item, 1u);
+      item = __shfl_sync(kFull, item, 0);
+      if (item >= nitem) break;
+      if (item < a.nmed_warp) {
+        const uint32_t p = a.mp[item];
+        uint32_t s;
+        const uint64_t q0 = first_hit(p, a.mm[item], x, a.p2_floor ? p : 2, s);
+        if (q0 < S) {
+          const uint64_t q = q0 + (uint64_t)p * (c_cum[s][lane & 7] + 15u * (lane >> 3));
+          const uint32_t step = 60u * p;
+          if (q < S)
+            for (uint32_t qq = (uint32_t)q; qq < S; qq += step) atomicOr(&tile[qq >> 5], 1u << (qq & 31));
+        }
+      } else {
+        const uint32_t i = a.nmed_warp + (item - a.nmed_warp) * 32 + lane;
+        if (i < a.nmed) {
+          const uint32_t p = a.mp[i];
+          uint32_t s;
+          const uint64_t q0 = first_hit(p, a.mm[i], x, a.p2_floor ? p : 2, s);
+          if (q0 < S) {
+            uint32_t q = (uint32_t)q0;
+            while (q < S) {
+              atomicOr(&tile[q >> 5], 1u << (q & 31));
+              q += wheel_D(s) * p;
+              s = (s + 1) & 7;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  // 3. large primes: this tile's hit records
+  if (a.hits) {
+    const uint32_t cnt = min(a.hitcnt[blockIdx.x], a.hcap);
+    const uint32_t* h = a.hits + (uint64_t)blockIdx.x * a.hcap;
+    const uint32_t n4 = cnt >> 2;
+    const uint4* h4 = reinterpret_cast<const uint4*>(h);
+    for (uint32_t i = tid; i < n4; i += bd) {
+      const uint4 v = h4[i];
+      atomicOr(&tile[v.x >> 5], 1u << (v.x & 31));
+      atomicOr(&tile[v.y >> 5], 1u << (v.y & 31));
+      atomicOr(&tile[v.z >> 5], 1u << (v.z & 31));
+      atomicOr(&tile[v.w >> 5], 1u << (v.w & 31));
+    }
+    for (uint32_t i = (n4 << 2) + tid; i < cnt; i += bd) {
+      const uint32_t q = h[i];
+      atomicOr(&tile[q >> 5], 1u << (q & 31));
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (a.hits) a.hitcnt[blockIdx.x] = 0;
+    if (blockIdx.x == 0 && a.reset_bucket_count) *a.reset_bucket_count = 0;
+  }
+
+  // 4. popcount + write-out (count_zeros simd.cpp:18-25, segment_to_bytes
+  // driver.cpp:22-27: LSB-first bytes == little-endian words)
+  const uint64_t rem = a.tbits - tstart;
+  const uint32_t valid = rem < S ? (uint32_t)rem : S;  // multiple of 16
+  const uint32_t vbytes = valid >> 3;
+  unsigned long long ones = 0;
+  uint32_t* out = a.table ? a.table + (tstart >> 5) : nullptr;
+  for (uint32_t w4 = tid; w4 < (nw >> 2); w4 += bd) {
+    const uint32_t w0 = w4 << 2;
+    if (w0 * 32 >= valid) break;
+    uint4 v = smem4[kPatWords / 4 + w4];
+    if ((w0 + 4) * 32 > valid) {  // partial quad at the end of the run
+      uint32_t* e = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t lo = (w0 + k) * 32;
+        if (lo >= valid) e[k] = 0;
+        else if (valid - lo < 32) e[k] &= (1u << (valid - lo)) - 1;
+      }
+      if (out) {
+        uint8_t* ob = reinterpret_cast<uint8_t*>(out + w0);
+        const uint8_t* vb = reinterpret_cast<const uint8_t*>(&v);
+        for (uint32_t b = 0; b < 16 && w0 * 4 + b < vbytes; ++b) ob[b] = vb[b];
+      }
+    } else if (out) {
+      __stcs(reinterpret_cast<uint4*>(out + w0), v);
+    }
+    ones += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  for (int o = 16; o; o >>= 1) ones += __shfl_xor_sync(kFull, ones, o);
+  if (lane == 0) s_red[warp] = ones;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long t = lane < (bd >> 5) ? s_red[lane] : 0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+    if (lane == 0) atomicAdd(a.count, (unsigned long long)valid - t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Large-prime scatter for one wave (W tiles, WS = W*S bits).
+//  * ML entries (S < p <= WS; several hits per wave): a flat array in prime
+//    order, visited every wave.  Encoding: lo32 = q (index offset of the next
+//    hit from the current wave start), hi32 = p | s<<29.
+//  * far entries (p > WS; at most one hit per wave): a ring of per-wave
+//    buckets; bucket w holds exactly the entries whose next hit lies in wave
+//    w.  Encoding: lo32 = p, hi32 = q | s<<29 (q < WS < 2^29).
+// Each visit emits hit records (offset inside the tile) into per-tile lists,
+// staged per CTA through shared-memory counters (two passes: count, reserve
+// with one global atomic per tile, write), and re-buckets far entries with
+// warp-aggregated appends (__match_any_sync on the target slot).
+struct ScatterArgs {
+  uint64_t* ml;
+  uint32_t nml;
+  uint32_t ml_blocks;           // CTAs [0, ml_blocks) do ML, the rest far
+  const uint64_t* far_in;       // bucket of this wave
+  const uint32_t* far_in_count;
+  uint64_t* buckets;  // [ring][bcap]
+  uint32_t* bcount;   // [ring]
+  uint32_t ring, bcap;
+  uint64_t wave, nwaves;
+  uint32_t ntiles_w;  // tiles in this wave (<= W)
+  uint32_t log_s;
+  uint32_t WS;        // wave span in bits (<= 2^29)
+  double inv_ws;
+  uint32_t* hits;     // [W][hcap]
+  uint32_t* hitcnt;   // [W]
+  uint32_t hcap;
+  int* overflow;
+};
+
+constexpr int kScatterThreads = 512;
+constexpr int kMaxWaveTiles = 1024;
+constexpr int kMlEPT = 4;
+constexpr int kFarEPT = 8;
+
+__device__ __forceinline__ void reserve_tiles(const ScatterArgs& a, uint32_t* s_cnt, uint32_t* s_base) {
+  for (uint32_t t = threadIdx.x; t < a.ntiles_w; t += blockDim.x) {
+    const uint32_t c = s_cnt[t];
+    if (c) {
+      const uint32_t b = atomicAdd(&a.hitcnt[t], c);
+      s_base[t] = b;
+      if (b + c > a.hcap) atomicExch(a.overflow, 1);
+    }
+    s_cnt[t] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kScatterThreads) k_scatter(const ScatterArgs a) {
+  __shared__ uint32_t s_cnt[kMaxWaveTiles];
+  __shared__ uint32_t s_base[kMaxWaveTiles];
+  const uint32_t tid = threadIdx.x, bd = blockDim.x;
+  const uint32_t S = 1u << a.log_s, smask = S - 1;
+  for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
+  __syncthreads();
+
+  if (blockIdx.x < a.ml_blocks) {
+    // ---------------- ML: several hits per wave ----------------
+    const uint32_t CH = bd * kMlEPT;
+    for (uint64_t base = (uint64_t)blockIdx.x * CH; base < a.nml; base += (uint64_t)a.ml_blocks * CH) {
+      uint64_t ent[kMlEPT];
+#pragma unroll
+      for (int k = 0; k < kMlEPT; ++k) {
+        const uint64_t e = base + tid + (uint64_t)k * bd;
+        ent[k] = e < a.nml ? a.ml[e] : ~0ull;
+        if (e < a.nml) {
+          uint32_t q = (uint32_t)ent[k];
+          const uint32_t hi = (uint32_t)(ent[k] >> 32);
+          const uint32_t p = hi & 0x1fffffffu;
+          uint32_t s = hi >> 29;
+          while (q < a.WS) {
+            const uint32_t t = q >> a.log_s;
+            if (t < a.ntiles_w) atomicAdd(&s_cnt[t], 1u);
+            q += wheel_D(s) * p;
+            s = (s + 1) & 7;
+          }
+        }
+      }
+      __syncthreads();
+      reserve_tiles(a, s_cnt, s_base);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kMlEPT; ++k) {
+        const uint64_t e = base + tid + (uint64_t)k * bd;
+        if (e < a.nml) {
+          uint32_t q = (uint32_t)ent[k];
+          const uint32_t hi = (uint32_t)(ent[k] >> 32);
+          const uint32_t p = hi & 0x1fffffffu;
+          uint32_t s = hi >> 29;
+          while (q < a.WS) {
+            const uint32_t t = q >> a.log_s;
+            if (t < a.ntiles_w) {
+              const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
+              if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = q & smask;
+            }
+            q += wheel_D(s) * p;
+            s = (s + 1) & 7;
+          }
+          a.ml[e] = (uint64_t)(q - a.WS) | ((uint64_t)(p | (s << 29)) << 32);
+        }
+      }
+      __syncthreads();
+      for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
+      __syncthreads();
+    }
+  } else {
+    // ---------------- far: exactly one hit in this wave ----------------
+    const uint32_t nfar = *a.far_in_count < a.bcap ? *a.far_in_count : a.bcap;
+    const uint32_t nb = gridDim.x - a.ml_blocks, b0 = blockIdx.x - a.ml_blocks;
+    const uint32_t CH = bd * kFarEPT;
+    const uint32_t lane = tid & 31;
+    for (uint64_t base = (uint64_t)b0 * CH; base < nfar; base += (uint64_t)nb * CH) {
+      uint64_t ent[kFarEPT];
+#pragma unroll
+      for (int k = 0; k < kFarEPT; ++k) {
+        const uint64_t e = base + tid + (uint64_t)k * bd;
+        ent[k] = e < nfar ? a.far_in[e] : ~0ull;
+        if (e < nfar) {
+          const uint32_t q = (uint32_t)(ent[k] >> 32) & 0x1fffffffu;
+          const uint32_t t = q >> a.log_s;
+          if (t < a.ntiles_w) atomicAdd(&s_cnt[t], 1u);
+        }
+      }
+      __syncthreads();
+      reserve_tiles(a, s_cnt, s_base);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kFarEPT; ++k) {
+        const uint64_t e = base + tid + (uint64_t)k * bd;
+        bool app = false;
+        uint32_t slotb = 0;
+        uint64_t nent = 0;
+        if (e < nfar) {
+          const uint32_t p = (uint32_t)ent[k];
+          const uint32_t hi = (uint32_t)(ent[k] >> 32);
+          const uint32_t q = hi & 0x1fffffffu;
+          const uint32_t s = hi >> 29;
+          const uint32_t t = q >> a.log_s;
+          if (t < a.ntiles_w) {
+            const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
+            if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = q & smask;
+            // next hit: k or k+1 waves ahead in the paper's sense (Lemma 2)
+            const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
+            uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
+            while (d * a.WS > q2) --d;
+            while ((d + 1) * a.WS <= q2) ++d;
+            const uint64_t tgt = a.wave + d;
+            if (tgt < a.nwaves) {
+              app = true;
+              slotb = (uint32_t)(tgt % a.ring);
+              nent = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * a.WS) | (((s + 1) & 7) << 29)) << 32);
+            }
+          }
+        }
+        const uint32_t part = __ballot_sync(kFull, app);
+        if (app) {
+          const uint32_t grp = __match_any_sync(part, slotb);
+          const uint32_t leader = __ffs(grp) - 1;
+          uint32_t b = 0;
+          if (lane == leader) b = atomicAdd(&a.bcount[slotb], (uint32_t)__popc(grp));
+          b = __shfl_sync(grp, b, leader);
+          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
+          if (pos < a.bcap) a.buckets[(uint64_t)slotb * a.bcap + pos] = nent;
+          else atomicExch(a.overflow, 1);
+        }
+      }
+      __syncthreads();
+      for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Base primes: odd primes < 2^16 in one CTA (sieve in smem + block compaction).
+__global__ void __launch_bounds__(1024) k_small_primes(uint32_t* __restrict__ out, uint32_t* __restrict__ count) {
+  __shared__ uint32_t bits[1024];  // 32768 odd numbers 1..65535
+  __shared__ uint32_t s_scan[1024];
+  const uint32_t tid = threadIdx.x;
+  bits[tid] = tid == 0 ? 1u : 0u;  // number 1 is not prime
+  __syncthreads();
+  for (uint32_t i = 3; i * i < 65536; i += 2) {
+    if (!((bits[i >> 6] >> ((i >> 1) & 31)) & 1)) {
+      for (uint32_t j = i * i + 2 * i * tid; j < 65536; j += 2 * i * blockDim.x)
+        atomicOr(&bits[j >> 6], 1u << ((j >> 1) & 31));
+    }
+    __syncthreads();
+  }
+  const uint32_t free_bits = ~bits[tid];
+  const uint32_t c = __popc(free_bits);
+  s_scan[tid] = c;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {
+    const uint32_t v = tid >= o ? s_scan[tid - o] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  uint32_t pos = s_scan[tid] - c;
+  uint32_t fb = free_bits;
+  while (fb) {
+    const uint32_t b = __ffs(fb) - 1;
+    fb &= fb - 1;
+    out[pos++] = 2 * (tid * 32 + b) + 1;
+  }
+  if (tid == 1023) *count = s_scan[1023];
+}
+
+__global__ void k_barrett(const uint32_t* __restrict__ p, uint64_t* __restrict__ m, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) m[i] = ~0ull / p[i];
+}
+
+// ---- compaction of a bit table to the sorted list of its zero bits ---------
+// Block = 1024 words (32768 bits).  Zero bit j (lo <= j < nbits) -> value
+// base + 2*j (u64) or 2*j+1 (u32 base primes).
+constexpr int kCompactWords = 1024;
+
+__global__ void __launch_bounds__(1024) k_count_zeros_blocks(const uint32_t* __restrict__ bits, uint64_t nbits,
+                                                            uint64_t lo, uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t s_red[32];
+  const uint64_t w = (uint64_t)blockIdx.x * kCompactWords + threadIdx.x;
+  uint32_t c = 0;
+  if (w * 32 < nbits) {
+    uint32_t v = ~bits[w];
+    const uint64_t b0 = w * 32;
+    if (nbits - b0 < 32) v &= (1u << (nbits - b0)) - 1;
+    if (b0 < lo) v &= lo - b0 >= 32 ? 0u : ~((1u << (lo - b0)) - 1);
+    c = __popc(v);
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t t = s_red[threadIdx.x];
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of n u32 counts into u64 offsets (single CTA); total -> *total
+__global__ void __launch_bounds__(1024) k_scan_counts(const uint32_t* __restrict__ c, uint32_t n,
+                                                     uint64_t* __restrict__ off, uint64_t* __restrict__ total) {
+  __shared__ uint64_t s[1024];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t b = tid * per, e = min(n, b + per);
+  uint64_t sum = 0;
+  for (uint32_t i = b; i < e; ++i) sum += c[i];
+  s[tid] = sum;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {
+    const uint64_t v = tid >= o ? s[tid - o] : 0;
+    __syncthreads();
+    s[tid] += v;
+    __syncthreads();
+  }
+  uint64_t run = s[tid] - sum;
+  for (uint32_t i = b; i < e; ++i) {
+    off[i] = run;
+    run += c[i];
+  }
+  if (tid == 1023) *total = s[1023];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_write_zeros(const uint32_t* __restrict__ bits, uint64_t nbits, uint64_t lo,
+                                                     const uint64_t* __restrict__ boff, uint64_t base,
+                                                     T* __restrict__ out, uint64_t cap) {
+  __shared__ uint32_t s_scan[1024];
+  const uint32_t tid = threadIdx.x;
+  const uint64_t w = (uint64_t)blockIdx.x * kCompactWords + tid;
+  uint32_t v = 0;
+  if (w * 32 < nbits) {
+    v = ~bits[w];
+    const uint64_t b0 = w * 32;
+    if (nbits - b0 < 32) v &= (1u << (nbits - b0)) - 1;
+    if (b0 < lo) v &= lo - b0 >= 32 ? 0u : ~((1u << (lo - b0)) - 1);
+  }
+  const uint32_t c = __popc(v);
+  s_scan[tid] = c;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {
+    const uint32_t x = tid >= o ? s_scan[tid - o] : 0;
+    __syncthreads();
+    s_scan[tid] += x;
+    __syncthreads();
+  }
+  uint64_t pos = boff[blockIdx.x] + s_scan[tid] - c;
+  while (v) {
+    const uint32_t b = __ffs(v) - 1;
+    v &= v - 1;
+    if (pos < cap) out[pos] = (T)(base + 2 * (w * 32 + b));
+    ++pos;
+  }
+}
+
+// number of entries of a sorted array <= x, for several thresholds
+__global__ void k_bounds(const uint32_t* __restrict__ p, const uint64_t* __restrict__ n_ptr,
+                         const uint64_t* __restrict__ thr, int nthr, uint64_t* __restrict__ out) {
+  const int i = threadIdx.x;
+  if (i >= nthr) return;
+  const uint64_t n = *n_ptr, x = thr[i];
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if ((uint64_t)p[mid] <= x) lo = mid + 1;
+    else hi = mid;
+  }
+  out[i] = lo;
+}
+
+// ---- large-prime setup: first hits, ML array, initial far buckets ---------
+struct SetupArgs {
+  const uint32_t* primes;
+  uint64_t i0, i_ml_end, i_end;  // ML = [i0, i_ml_end), far = [i_ml_end, i_end)
+  uint64_t x0;                   // 2*g0 + 1
+  uint64_t* ml;
+  uint64_t* buckets;
+  uint32_t* bcount;
+  uint32_t ring, bcap;
+  uint64_t nwaves;
+  uint32_t WS;
+  double inv_ws;
+  int* overflow;
+};
+
+__global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
+  const uint64_t i = a.i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31;
+  bool app = false;
+  uint32_t slotb = 0;
+  uint64_t nent = 0;
+  if (i < a.i_end) {
+    const uint32_t p = a.primes[i];
+    uint32_t s;
+    // cofactor >= 2 (-> >= 7 after the wheel): never marks p itself, keeps
+    // the first hit within 3.5p of the interval start in overlap runs.
+    const uint64_t pos = first_hit(p, ~0ull / p, a.x0, 2, s);
+    if (i < a.i_ml_end) {
+      a.ml[i - a.i0] = (uint64_t)(uint32_t)pos | ((uint64_t)(p | (s << 29)) << 32);
+    } else {
+      uint64_t d = (uint64_t)((double)pos * a.inv_ws);
+      while (d * a.WS > pos) --d;
+      while ((d + 1) * a.WS <= pos) ++d;
+      if (d < a.nwaves) {
+        app = true;
+        slotb = (uint32_t)(d % a.ring);
+        nent = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
+      }
+    }
+  }
+  const uint32_t part = __ballot_sync(kFull, app);
+  if (app) {
+    const uint32_t grp = __match_any_sync(part, slotb);
+    const uint32_t leader = __ffs(grp) - 1;
+    uint32_t b = 0;
+    if (lane == leader) b = atomicAdd(&a.bcount[slotb], (uint32_t)__popc(grp));
+    b = __shfl_sync(grp, b, leader);
+    const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
+    if (pos < a.bcap) a.buckets[(uint64_t)slotb * a.bcap + pos] = nent;
+    else atomicExch(a.overflow, 1);
+  }
+}
+
+}  // namespace eg
