@@ -51,6 +51,8 @@ enum {
 #define ERATO_GPU_TEST_MODE 0x1u     /* l >= 4 instead of 10 (params.hpp:58-60) */
 #define ERATO_GPU_ALLOW_OVERLAP 0x2u /* accept u^2 <= v incl. f = 0 (SURVEY §8c convention:
                                         multiples from max(u, p^2); 1 and primes stay 0) */
+#define ERATO_GPU_PHASE_TIMING 0x100u /* CUDA events around every launch: fills small_s (tile
+                                         kernel) and large_s (bucket scatter) in the stats */
 
 /* RunStats (driver.hpp:24-32).  Times are seconds of device time (CUDA
  * events); small_s covers masks+medium (tile kernel), large_s the bucket

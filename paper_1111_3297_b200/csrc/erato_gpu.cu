@@ -92,12 +92,13 @@ struct erato_gpu_ctx {
   int nsm = 0;
   cudaStream_t stream = nullptr;
   // cached per context
-  DevBuf sp, spm, ptab;  // small primes < 2^16, their Barrett constants, pattern tables
+  DevBuf sp, spm, ptab;  // small primes < 2^16, their base-sieve records, pattern tables
   std::vector<uint32_t> h_sp;
   // grow-only run buffers
-  DevBuf base_bits, primes, mm, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
+  DevBuf base_bits, primes, med, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
   double hcap_scale = 1.0, bcap_scale = 1.0;
   cudaEvent_t ev[4] = {};
+  std::vector<cudaEvent_t> phase_ev;  // pairs, grown on demand
 };
 
 extern "C" {
@@ -209,7 +210,7 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
                                 (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
-  CUDA_TRY(c->spm.ensure(8192 * 8));
+  CUDA_TRY(c->spm.ensure(8192 * 16));
   CUDA_TRY(c->ptab.ensure(eg::kPatWords * 4));
   CUDA_TRY(c->scal.ensure(64 * 8));
   eg::k_build_patterns<<<(eg::kPatWords + 255) / 256, 256, 0, c->stream>>>(c->ptab.as<uint32_t>());
@@ -217,7 +218,9 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   uint32_t nsp = 0;
   CUDA_TRY(cudaMemcpyAsync(&nsp, c->scal.p, 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  eg::k_barrett<<<(nsp + 255) / 256, 256, 0, c->stream>>>(c->sp.as<uint32_t>(), c->spm.as<uint64_t>(), nsp);
+  // base-sieve records: g0 = 0 (x0 = 1), tiles of 2^kBaseLogTile bits
+  eg::k_med_records<<<(nsp + 255) / 256, 256, 0, c->stream>>>(c->sp.as<uint32_t>(), nsp, 1, kBaseLogTile,
+                                                              c->spm.as<uint4>());
   c->h_sp.resize(nsp);
   CUDA_TRY(cudaMemcpyAsync(c->h_sp.data(), c->sp.p, nsp * 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -229,12 +232,13 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
 void erato_gpu_destroy(erato_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->mm, &c->ml, &c->buckets,
+  for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
                     &c->outbuf})
     b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->phase_ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -341,8 +345,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ta.tbits = nbase_bits;
       ta.tile0 = 0;
       ta.log_s = kBaseLogTile;
-      ta.mp = c->sp.as<uint32_t>() + b61;
-      ta.mm = c->spm.as<uint64_t>() + b61;
+      ta.med = c->spm.as<uint4>() + b61;
       ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
       {
         const auto bw = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), (1u << kBaseLogTile) / 64) - c->h_sp.begin();
@@ -379,10 +382,10 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
 
     // ---------------- 4. medium constants + large-prime structures ----------------
     const uint64_t nmed = iS - i61, nml = iWS - iS, nfar = nprimes - iWS;
-    CUDA_TRY(c->mm.ensure(std::max<uint64_t>(nmed, 1) * 8));
+    CUDA_TRY(c->med.ensure(std::max<uint64_t>(nmed, 1) * 16));
     if (nmed)
-      eg::k_barrett<<<(unsigned)((nmed + 255) / 256), 256, 0, st>>>(c->primes.as<uint32_t>() + i61, c->mm.as<uint64_t>(),
-                                                                     (uint32_t)nmed);
+      eg::k_med_records<<<(unsigned)((nmed + 255) / 256), 256, 0, st>>>(c->primes.as<uint32_t>() + i61, (uint32_t)nmed,
+                                                                         2 * P.g0 + 1, P.log_s, c->med.as<uint4>());
     ++launches;
     const bool have_large = nml + nfar > 0;
     uint32_t ring = 1, bcap = 1, hcap = 4;
@@ -436,8 +439,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.g0 = P.g0;
     ta.tbits = P.T;
     ta.log_s = P.log_s;
-    ta.mp = c->primes.as<uint32_t>() + i61;
-    ta.mm = c->mm.as<uint64_t>();
+    ta.med = c->med.as<uint4>();
     ta.nmed = (uint32_t)nmed;
     ta.nmed_warp = (uint32_t)std::min<uint64_t>(iwarp - i61, nmed);
     ta.ptab = c->ptab.as<uint32_t>();
@@ -469,6 +471,13 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sc.overflow = reinterpret_cast<int*>(d_scal + 17);
     }
     const uint32_t far_blocks = nfar ? (uint32_t)c->nsm * 2 : 0;
+    const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
+    const size_t nev = timing ? (size_t)P.nwaves * 4 : 0;
+    while (c->phase_ev.size() < nev) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      c->phase_ev.push_back(e);
+    }
     for (uint64_t w = 0; w < P.nwaves; ++w) {
       const uint64_t tile0 = w * P.W;
       const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
@@ -478,12 +487,16 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         const uint32_t slot = nfar ? (uint32_t)(w % ring) : 0;
         sc.far_in = c->buckets.as<uint64_t>() + (uint64_t)slot * bcap;
         sc.far_in_count = c->bcount.as<uint32_t>() + slot;
+        if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[4 * w], st));
         eg::k_scatter<<<sc.ml_blocks + far_blocks, eg::kScatterThreads, 0, st>>>(sc);
+        if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[4 * w + 1], st));
         ++launches;
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
       ta.tile0 = tile0;
+      if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[4 * w + 2], st));
       launch_tiles(c, st, ta, ntw);
+      if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[4 * w + 3], st));
       ++launches;
     }
     CUDA_TRY(cudaGetLastError());
@@ -522,6 +535,18 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       stats->segments = n;
       stats->init_s = t_init * 1e-3;
       stats->small_s = (t_tot - t_init) * 1e-3;
+      if (timing) {
+        double ts = 0, tl = 0;
+        for (uint64_t w = 0; w < P.nwaves; ++w) {
+          float a = 0, b = 0;
+          if (have_large) cudaEventElapsedTime(&a, c->phase_ev[4 * w], c->phase_ev[4 * w + 1]);
+          cudaEventElapsedTime(&b, c->phase_ev[4 * w + 2], c->phase_ev[4 * w + 3]);
+          tl += a;
+          ts += b;
+        }
+        stats->small_s = ts * 1e-3;
+        stats->large_s = tl * 1e-3;
+      }
       stats->total_s = t_tot * 1e-3;
       stats->base_primes = nprimes;
       stats->tiles = P.ntiles;

@@ -11,8 +11,8 @@
 // Prime classes (GPU split; the reference's split is base.cpp:11-17):
 //   small   p <= 61        periodic word patterns (masks.cpp:9-50 idea)
 //   medium  61 < p <= S    shared-memory atomicOr marking inside the tile,
-//                          start offset recomputed per tile (64-bit Barrett,
-//                          __umul64hi), mod-30 wheel over the cofactor
+//                          start offset recomputed per tile from 32-bit
+//                          residues (MedRecs), mod-30 wheel over the cofactor
 //                          (wheel.cpp:10-69 idea: 8 of 15 odd cofactors)
 //   large   p > S          bucketed: (p,q) entries scattered into the wave
 //                          of their next hit, which emits per-tile hit
@@ -118,14 +118,41 @@ __global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
 }
 
 // ---------------------------------------------------------------------------
-// Tile kernel: one CTA = one S-bit tile in shared memory.
+// Medium-prime record, one per prime per run (16 B, read by every tile):
+//   x    p | inv30(p) << 24         (p < 2^24; inv30 = p^-1 mod 30)
+//   y    r0  = (2*g0 + 1) mod p     (residue of the run's first odd number)
+//   z    rho = (2*S) mod p          (residue step per tile)
+//   w    float 1/p                  (quotient estimate for (t*rho) mod p)
+// Tile t then needs only 32-bit work: r_t = (r0 + t*rho) mod p gives the
+// first multiple c*p >= x_t = 2*(g0 + t*S) + 1, and the cofactor class is
+// c = (x_t + d) * p^-1 (mod 30) — no 64-bit division per (prime, tile).
+struct MedRecs {
+  const uint4* rec;
+  uint32_t n;
+};
+
+__global__ void k_med_records(const uint32_t* __restrict__ primes, uint32_t n, uint64_t x0, uint32_t log_s,
+                              uint4* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t p = primes[i];
+  const uint32_t pm = p % 30u;
+  // p^-1 mod 30 for the 8 residues coprime to 30
+  const uint32_t inv = pm == 1 ? 1 : pm == 7 ? 13 : pm == 11 ? 11 : pm == 13 ? 7 : pm == 17 ? 23 : pm == 19 ? 19
+                     : pm == 23 ? 17 : 29;
+  out[i] = make_uint4(p | (inv << 24), (uint32_t)(x0 % p), (uint32_t)(((uint64_t)2 << log_s) % p),
+                      __float_as_uint(1.0f / (float)p));
+}
+
+// combo[cm] = adv | cls << 3 ; cum4[s] = nibbles cum[s][0..7]
+__device__ __forceinline__ uint32_t nib(uint32_t packed, uint32_t k) { return (packed >> (k << 2)) & 15u; }
+
 struct TileArgs {
   uint64_t g0;     // global odd index of table bit 0 (= f << l)
   uint64_t tbits;  // table bits T of this run (shard)
   uint64_t tile0;  // first tile of this launch
   uint32_t log_s;
-  const uint32_t* mp;  // medium primes (61 < p <= S, <= sqrt(v)), ascending
-  const uint64_t* mm;  // floor((2^64-1)/p)
+  const uint4* med;      // medium-prime records (61 < p <= S), ascending p
   uint32_t nmed;
   uint32_t nmed_warp;    // the first nmed_warp medium primes are marked warp-per-prime
   const uint32_t* ptab;  // kPatWords pattern words (global)
@@ -135,29 +162,64 @@ struct TileArgs {
   uint32_t* table;               // output words (nullable: count only)
   unsigned long long* count;     // zero-bit accumulator
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
-  int p2_floor;                  // 1: medium multiples from p^2 (overlap runs, base sieve)
+  int p2_floor;                  // 1: multiples from p^2 (overlap runs, base sieve)
 };
 
 constexpr int kTileThreads = 1024;
+constexpr int kTileWarps = kTileThreads / 32;
+
+__device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
+
+// First admissible multiple of a medium prime in tile t (see MedRecs).
+// Returns the index offset from the tile start (may be >= S) and class s.
+__device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, uint32_t X30, uint64_t x_t,
+                                              bool early, const uint8_t* combo, uint32_t& p, uint32_t& s) {
+  p = rec.x & 0xffffffu;
+  const uint32_t inv30 = rec.x >> 24;
+  // (t * rho) mod p with an fp32 quotient estimate (|error| <= 2)
+  const uint32_t qe = (uint32_t)__fmul_rz(__uint2float_rz(t), __fmul_rz(__uint2float_rz(rec.z), __uint_as_float(rec.w)));
+  int32_t rem = (int32_t)(t * rec.z - qe * p);
+  if (rem < 0) rem += p;
+  if (rem >= (int32_t)p) rem -= p;
+  if (rem >= (int32_t)p) rem -= p;
+  uint32_t r = rec.y + (uint32_t)rem;
+  if (r >= p) r -= p;
+  uint32_t d = r ? p - r : 0;  // c1*p - x_t, c1 = ceil(x_t/p)
+  if (early && x_t + d < (uint64_t)p * p) {  // p^2 floor (overlap runs); far floors only need q0 >= S
+    const uint64_t dd = (uint64_t)p * p - x_t;
+    d = dd < (1u << 30) ? (uint32_t)dd : (1u << 30);
+  }
+  const uint32_t cm = ((X30 + d % 30u) * inv30) % 30u;
+  const uint32_t cb = combo[cm];
+  s = cb >> 3;
+  return (d + (cb & 7u) * p) >> 1;
+}
 
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   extern __shared__ uint4 smem4[];
   uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
   uint32_t* const tile = pat + kPatWords;
-  __shared__ uint32_t s_item;
-  __shared__ unsigned long long s_red[kTileThreads / 32];
+  __shared__ unsigned long long s_red[kTileWarps];
+  __shared__ uint8_t s_combo[32];
+  __shared__ uint32_t s_cum[8];
 
   const uint32_t tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t log_s = a.log_s;
   const uint32_t S = 1u << log_s, nw = S >> 5;
-  const uint64_t tstart = (a.tile0 + blockIdx.x) << log_s;
+  const uint64_t t64 = a.tile0 + blockIdx.x;
+  const uint64_t tstart = t64 << log_s;
   const uint64_t g = a.g0 + tstart;
 
-  {  // stage pattern tables
+  {  // stage pattern tables and the wheel tables
     const uint4* src = reinterpret_cast<const uint4*>(a.ptab);
     for (uint32_t i = tid; i < kPatWords / 4; i += bd) smem4[i] = src[i];
+    if (tid < 30) s_combo[tid] = (uint8_t)(c_adv[tid] | (c_cls[tid + c_adv[tid]] << 3));
+    if (tid < 8) {
+      uint32_t v = 0;
+      for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
+      s_cum[tid] = v;
+    }
   }
-  if (tid == 0) s_item = 0;
   __syncthreads();
 
   // 1. small primes: OR of the 8 group windows, plain stores
@@ -191,41 +253,65 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     }
   }
 
-  // 2. medium primes, dynamic work list: warp-per-prime items first (most
-  // marks), then 32-primes-per-warp items.
+  // 2. medium primes
   {
-    const uint64_t x = 2 * g + 1;
-    const uint32_t nitem = a.nmed_warp + (a.nmed - a.nmed_warp + 31) / 32;
-    for (;;) {
-      uint32_t item = 0;
-      if (lane == 0) item = atomicAdd(&s_item, 1u);
-      item = __shfl_sync(kFull, item, 0);
-      if (item >= nitem) break;
-      if (item < a.nmed_warp) {
-        const uint32_t p = a.mp[item];
-        uint32_t s;
-        const uint64_t q0 = first_hit(p, a.mm[item], x, a.p2_floor ? p : 2, s);
-        if (q0 < S) {
-          const uint64_t q = q0 + (uint64_t)p * (c_cum[s][lane & 7] + 15u * (lane >> 3));
-          const uint32_t step = 60u * p;
-          if (q < S)
-            for (uint32_t qq = (uint32_t)q; qq < S; qq += step) atomicOr(&tile[qq >> 5], 1u << (qq & 31));
+    const uint64_t x_t = 2 * g + 1;
+    const uint32_t X30 = (uint32_t)(x_t % 30u);
+    const uint32_t t = (uint32_t)t64;
+    const bool early = a.p2_floor && x_t < ((uint64_t)1 << 42);
+    // 2a. warp-per-prime (p < S/64): lane j takes wheel class (s+j)&7 of
+    // period j>>3; 32 lanes = 4 periods = 60p.  Items in snake order over
+    // the warps (largest work first) for balance.
+    for (uint32_t r = 0;; ++r) {
+      const uint32_t item = r * kTileWarps + ((r & 1) ? (kTileWarps - 1 - warp) : warp);
+      if (item >= a.nmed_warp) break;
+      uint32_t p, s;
+      const uint32_t q0 = med_first(a.med[item], t, X30, x_t, early, s_combo, p, s);
+      uint32_t q = q0 + p * (nib(s_cum[s], lane & 7) + 15u * (lane >> 3));
+      const uint32_t step = 60u * p;
+      for (; q + 3 * step < S; q += 4 * step) {
+        mark(tile, q);
+        mark(tile, q + step);
+        mark(tile, q + 2 * step);
+        mark(tile, q + 3 * step);
+      }
+      for (; q < S; q += step) mark(tile, q);
+    }
+    // 2b. lane-per-prime (S/64 <= p <= S): whole wheel periods unrolled
+    const uint32_t nlane = a.nmed - a.nmed_warp;
+    const uint32_t nitem = (nlane + 31) / 32;
+    uint32_t item = warp;
+    uint4 rec = make_uint4(0, 0, 0, 0);
+    if (item < nitem && item * 32 + lane < nlane) rec = a.med[a.nmed_warp + item * 32 + lane];
+    for (; item < nitem; item += kTileWarps) {
+      const uint4 cur = rec;
+      const bool valid = item * 32 + lane < nlane;
+      const uint32_t nx = item + kTileWarps;
+      if (nx < nitem && nx * 32 + lane < nlane) rec = a.med[a.nmed_warp + nx * 32 + lane];
+      if (valid) {
+        uint32_t p, s;
+        uint32_t q = med_first(cur, t, X30, x_t, early, s_combo, p, s);
+        const uint32_t cp = s_cum[s];
+        const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
+                       o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
+        const uint32_t per = 15u * p;
+        for (; q + o7 < S; q += per) {
+          mark(tile, q);
+          mark(tile, q + o1);
+          mark(tile, q + o2);
+          mark(tile, q + o3);
+          mark(tile, q + o4);
+          mark(tile, q + o5);
+          mark(tile, q + o6);
+          mark(tile, q + o7);
         }
-      } else {
-        const uint32_t i = a.nmed_warp + (item - a.nmed_warp) * 32 + lane;
-        if (i < a.nmed) {
-          const uint32_t p = a.mp[i];
-          uint32_t s;
-          const uint64_t q0 = first_hit(p, a.mm[i], x, a.p2_floor ? p : 2, s);
-          if (q0 < S) {
-            uint32_t q = (uint32_t)q0;
-            while (q < S) {
-              atomicOr(&tile[q >> 5], 1u << (q & 31));
-              q += wheel_D(s) * p;
-              s = (s + 1) & 7;
-            }
-          }
-        }
+        if (q < S) mark(tile, q);
+        if (q + o1 < S) mark(tile, q + o1);
+        if (q + o2 < S) mark(tile, q + o2);
+        if (q + o3 < S) mark(tile, q + o3);
+        if (q + o4 < S) mark(tile, q + o4);
+        if (q + o5 < S) mark(tile, q + o5);
+        if (q + o6 < S) mark(tile, q + o6);
       }
     }
   }
@@ -238,15 +324,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     const uint4* h4 = reinterpret_cast<const uint4*>(h);
     for (uint32_t i = tid; i < n4; i += bd) {
       const uint4 v = h4[i];
-      atomicOr(&tile[v.x >> 5], 1u << (v.x & 31));
-      atomicOr(&tile[v.y >> 5], 1u << (v.y & 31));
-      atomicOr(&tile[v.z >> 5], 1u << (v.z & 31));
-      atomicOr(&tile[v.w >> 5], 1u << (v.w & 31));
+      mark(tile, v.x);
+      mark(tile, v.y);
+      mark(tile, v.z);
+      mark(tile, v.w);
     }
-    for (uint32_t i = (n4 << 2) + tid; i < cnt; i += bd) {
-      const uint32_t q = h[i];
-      atomicOr(&tile[q >> 5], 1u << (q & 31));
-    }
+    for (uint32_t i = (n4 << 2) + tid; i < cnt; i += bd) mark(tile, h[i]);
   }
   __syncthreads();
   if (tid == 0) {
@@ -266,17 +349,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     if (w0 * 32 >= valid) break;
     uint4 v = smem4[kPatWords / 4 + w4];
     if ((w0 + 4) * 32 > valid) {  // partial quad at the end of the run
-      uint32_t* e = reinterpret_cast<uint32_t*>(&v);
+      uint32_t e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t lo = (w0 + k) * 32;
         if (lo >= valid) e[k] = 0;
         else if (valid - lo < 32) e[k] &= (1u << (valid - lo)) - 1;
       }
+      v = make_uint4(e[0], e[1], e[2], e[3]);
       if (out) {
         uint8_t* ob = reinterpret_cast<uint8_t*>(out + w0);
-        const uint8_t* vb = reinterpret_cast<const uint8_t*>(&v);
-        for (uint32_t b = 0; b < 16 && w0 * 4 + b < vbytes; ++b) ob[b] = vb[b];
+        for (uint32_t b = 0; b < 16 && w0 * 4 + b < vbytes; ++b) ob[b] = (uint8_t)(e[b >> 2] >> (8 * (b & 3)));
       }
     } else if (out) {
       __stcs(reinterpret_cast<uint4*>(out + w0), v);
@@ -287,9 +370,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   if (lane == 0) s_red[warp] = ones;
   __syncthreads();
   if (warp == 0) {
-    unsigned long long t = lane < (bd >> 5) ? s_red[lane] : 0;
-    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
-    if (lane == 0) atomicAdd(a.count, (unsigned long long)valid - t);
+    unsigned long long tsum = lane < (bd >> 5) ? s_red[lane] : 0;
+    for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(kFull, tsum, o);
+    if (lane == 0) atomicAdd(a.count, (unsigned long long)valid - tsum);
   }
 }
 
