@@ -377,44 +377,158 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Large-prime scatter for one wave (W tiles, WS = W*S bits).
-//  * ML entries (S < p <= WS; several hits per wave): a flat array in prime
-//    order, visited every wave.  Encoding: lo32 = q (index offset of the next
-//    hit from the current wave start), hi32 = p | s<<29.
-//  * far entries (p > WS; at most one hit per wave): a ring of per-wave
-//    buckets; bucket w holds exactly the entries whose next hit lies in wave
-//    w.  Encoding: lo32 = p, hi32 = q | s<<29 (q < WS < 2^29).
-// Each visit emits hit records (offset inside the tile) into per-tile lists,
-// staged per CTA through shared-memory counters (two passes: count, reserve
-// with one global atomic per tile, write), and re-buckets far entries with
-// warp-aggregated appends (__match_any_sync on the target slot).
+// Large primes (p > S).  The interval is cut into EPOCHS of E waves
+// (ES = E*W*S bits, ES < 2^32).  Once per epoch the scatter kernel walks
+// every large prime through the epoch and emits one 32-bit hit record (the
+// offset inside the tile) per wheel-admissible multiple into the list of
+// the tile it falls in; the tile kernels of the epoch's waves then consume
+// those lists.  This is the paper's bucket sort (large_kernel.hpp: each
+// (p,q) entry lands in the bucket of the segment it hits and the segment
+// consumes its bucket) with the bucket contents materialised as hit records,
+// because ~148 tiles are sieved at once and a prime below E*W*S hits many
+// of them.
+//   ML  (S < p <= ES): per-prime state, u64 = q | s << 61 (q = index offset
+//       of the next hit from the current epoch start), visited every epoch.
+//       dense ML (p <= ES/512) is walked warp-per-prime: lane j follows
+//       wheel class (s+j)&7 of period j>>3, so a warp's 32 lanes sit in
+//       ~60 different tiles and the smem counters see no contention.
+//   far (p > ES): at most one hit per epoch; bucketed by the epoch of its
+//       next hit (ring of epoch buckets, 16-byte entries {p | s<<32, q}).
+// Emission is a per-CTA counting sort: pass 1 counts hits per tile in
+// shared memory, one global atomicAdd per (CTA, tile) reserves a contiguous
+// slot range, pass 2 re-walks and writes.
 struct ScatterArgs {
-  uint64_t* ml;
-  uint32_t nml;
-  uint32_t ml_blocks;           // CTAs [0, ml_blocks) do ML, the rest far
-  const uint64_t* far_in;       // bucket of this wave
+  const uint32_t* ml_p;  // ML primes (ascending)
+  uint64_t* ml_state;    // q | s << 61
+  uint32_t nml, ndense;  // the first ndense ML primes are dense
+  const uint4* far_in;   // this epoch's far bucket
   const uint32_t* far_in_count;
-  uint64_t* buckets;  // [ring][bcap]
-  uint32_t* bcount;   // [ring]
+  uint4* far_buckets;  // [ring][bcap]
+  uint32_t* far_bcount;
   uint32_t ring, bcap;
-  uint64_t wave, nwaves;
-  uint32_t ntiles_w;  // tiles in this wave (<= W)
+  uint64_t epoch, nepochs;
+  uint64_t ES;          // epoch span in bits (< 2^32)
+  uint32_t ntiles_e;    // tiles in this epoch (<= kMaxEpochTiles)
   uint32_t log_s;
-  uint32_t WS;        // wave span in bits (<= 2^29)
-  double inv_ws;
-  uint32_t* hits;     // [W][hcap]
-  uint32_t* hitcnt;   // [W]
+  uint32_t* hits;       // [ntiles_e][hcap]
+  uint32_t* hitcnt;     // [ntiles_e]
   uint32_t hcap;
   int* overflow;
 };
 
 constexpr int kScatterThreads = 512;
-constexpr int kMaxWaveTiles = 1024;
-constexpr int kMlEPT = 4;
-constexpr int kFarEPT = 8;
+constexpr int kScatterWarps = kScatterThreads / 32;
+constexpr int kMaxEpochTiles = 4096;
 
-__device__ __forceinline__ void reserve_tiles(const ScatterArgs& a, uint32_t* s_cnt, uint32_t* s_base) {
-  for (uint32_t t = threadIdx.x; t < a.ntiles_w; t += blockDim.x) {
+template <bool kWrite>
+__device__ __forceinline__ void emit(const ScatterArgs& a, uint32_t* s_cnt, const uint32_t* s_base, uint64_t pos) {
+  const uint32_t t = (uint32_t)(pos >> a.log_s);
+  if (t < a.ntiles_e) {
+    if (!kWrite) {
+      atomicAdd(&s_cnt[t], 1u);
+    } else {
+      const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
+      if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = (uint32_t)pos & ((1u << a.log_s) - 1);
+    }
+  }
+}
+
+// One pass over this CTA's share of the epoch's large primes.
+template <bool kWrite>
+__device__ void scatter_pass(const ScatterArgs& a, uint32_t* s_cnt, const uint32_t* s_base, const uint32_t* s_cum) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t)blockIdx.x * kScatterWarps + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kScatterWarps;
+  const uint64_t ES = a.ES;
+  // dense ML: warp per prime
+  for (uint64_t i = gw; i < a.ndense; i += nw) {
+    const uint32_t p = a.ml_p[i];
+    const uint64_t st = a.ml_state[i];
+    const uint64_t q0 = st & ((1ull << 61) - 1);
+    const uint32_t s0 = (uint32_t)(st >> 61);
+    uint64_t pos = q0 + (uint64_t)p * (nib(s_cum[s0], lane & 7) + 15u * (lane >> 3));
+    const uint64_t step = 60ull * p;
+    for (; pos < ES; pos += step) emit<kWrite>(a, s_cnt, s_base, pos);
+    if (kWrite) {
+      // next hit = the smallest lane exit; its lane gives the class
+      const uint32_t ex = (uint32_t)(pos - ES);  // < 60p: fits u32 for dense primes
+      const uint32_t m = __reduce_min_sync(kFull, ex);
+      const uint32_t who = __ffs(__ballot_sync(kFull, ex == m)) - 1;
+      if (lane == 0) a.ml_state[i] = (uint64_t)m | ((uint64_t)((s0 + who) & 7) << 61);
+    }
+  }
+  // sparse ML: lane per prime
+  const uint64_t nsp = a.nml - a.ndense;
+  for (uint64_t b = gw * 32; b < nsp; b += nw * 32) {
+    const uint64_t i = a.ndense + b + lane;
+    if (i < a.nml) {
+      const uint32_t p = a.ml_p[i];
+      const uint64_t st = a.ml_state[i];
+      uint64_t pos = st & ((1ull << 61) - 1);
+      uint32_t s = (uint32_t)(st >> 61);
+      while (pos < ES) {
+        emit<kWrite>(a, s_cnt, s_base, pos);
+        pos += (uint64_t)wheel_D(s) * p;
+        s = (s + 1) & 7;
+      }
+      if (kWrite) a.ml_state[i] = (pos - ES) | ((uint64_t)s << 61);
+    }
+  }
+  // far: one hit, then re-bucket into the epoch of the next hit
+  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
+  for (uint64_t b = gw * 32; b < nfar; b += nw * 32) {
+    const uint64_t i = b + lane;
+    bool app = false;
+    uint32_t slotb = 0;
+    uint4 ne = make_uint4(0, 0, 0, 0);
+    if (i < nfar) {
+      const uint4 e = a.far_in[i];
+      const uint32_t p = e.x, s = e.y;
+      const uint64_t q = (uint64_t)e.z | ((uint64_t)e.w << 32);
+      emit<kWrite>(a, s_cnt, s_base, q);
+      if (kWrite) {
+        const uint64_t q2 = q + (uint64_t)wheel_D(s) * p;
+        const uint64_t d = q2 / ES;
+        const uint64_t tgt = a.epoch + d;
+        if (tgt < a.nepochs) {
+          app = true;
+          slotb = (uint32_t)(tgt % a.ring);
+          const uint64_t qn = q2 - d * ES;
+          ne = make_uint4(p, (s + 1) & 7, (uint32_t)qn, (uint32_t)(qn >> 32));
+        }
+      }
+    }
+    if (kWrite) {
+      const uint32_t part = __ballot_sync(kFull, app);
+      if (app) {
+        const uint32_t grp = __match_any_sync(part, slotb);
+        const uint32_t leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&a.far_bcount[slotb], (uint32_t)__popc(grp));
+        base = __shfl_sync(grp, base, leader);
+        const uint32_t pos = base + __popc(grp & ((1u << lane) - 1));
+        if (pos < a.bcap) a.far_buckets[(uint64_t)slotb * a.bcap + pos] = ne;
+        else atomicExch(a.overflow, 1);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kScatterThreads) k_scatter(const ScatterArgs a) {
+  __shared__ uint32_t s_cnt[kMaxEpochTiles];
+  __shared__ uint32_t s_base[kMaxEpochTiles];
+  __shared__ uint32_t s_cum[8];
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t t = tid; t < a.ntiles_e; t += blockDim.x) s_cnt[t] = 0;
+  if (tid < 8) {
+    uint32_t v = 0;
+    for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
+    s_cum[tid] = v;
+  }
+  __syncthreads();
+  scatter_pass<false>(a, s_cnt, s_base, s_cum);
+  __syncthreads();
+  for (uint32_t t = tid; t < a.ntiles_e; t += blockDim.x) {
     const uint32_t c = s_cnt[t];
     if (c) {
       const uint32_t b = atomicAdd(&a.hitcnt[t], c);
@@ -423,131 +537,8 @@ __device__ __forceinline__ void reserve_tiles(const ScatterArgs& a, uint32_t* s_
     }
     s_cnt[t] = 0;
   }
-}
-
-__global__ void __launch_bounds__(kScatterThreads) k_scatter(const ScatterArgs a) {
-  __shared__ uint32_t s_cnt[kMaxWaveTiles];
-  __shared__ uint32_t s_base[kMaxWaveTiles];
-  const uint32_t tid = threadIdx.x, bd = blockDim.x;
-  const uint32_t S = 1u << a.log_s, smask = S - 1;
-  for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
   __syncthreads();
-
-  if (blockIdx.x < a.ml_blocks) {
-    // ---------------- ML: several hits per wave ----------------
-    const uint32_t CH = bd * kMlEPT;
-    for (uint64_t base = (uint64_t)blockIdx.x * CH; base < a.nml; base += (uint64_t)a.ml_blocks * CH) {
-      uint64_t ent[kMlEPT];
-#pragma unroll
-      for (int k = 0; k < kMlEPT; ++k) {
-        const uint64_t e = base + tid + (uint64_t)k * bd;
-        ent[k] = e < a.nml ? a.ml[e] : ~0ull;
-        if (e < a.nml) {
-          uint32_t q = (uint32_t)ent[k];
-          const uint32_t hi = (uint32_t)(ent[k] >> 32);
-          const uint32_t p = hi & 0x1fffffffu;
-          uint32_t s = hi >> 29;
-          while (q < a.WS) {
-            const uint32_t t = q >> a.log_s;
-            if (t < a.ntiles_w) atomicAdd(&s_cnt[t], 1u);
-            q += wheel_D(s) * p;
-            s = (s + 1) & 7;
-          }
-        }
-      }
-      __syncthreads();
-      reserve_tiles(a, s_cnt, s_base);
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kMlEPT; ++k) {
-        const uint64_t e = base + tid + (uint64_t)k * bd;
-        if (e < a.nml) {
-          uint32_t q = (uint32_t)ent[k];
-          const uint32_t hi = (uint32_t)(ent[k] >> 32);
-          const uint32_t p = hi & 0x1fffffffu;
-          uint32_t s = hi >> 29;
-          while (q < a.WS) {
-            const uint32_t t = q >> a.log_s;
-            if (t < a.ntiles_w) {
-              const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
-              if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = q & smask;
-            }
-            q += wheel_D(s) * p;
-            s = (s + 1) & 7;
-          }
-          a.ml[e] = (uint64_t)(q - a.WS) | ((uint64_t)(p | (s << 29)) << 32);
-        }
-      }
-      __syncthreads();
-      for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
-      __syncthreads();
-    }
-  } else {
-    // ---------------- far: exactly one hit in this wave ----------------
-    const uint32_t nfar = *a.far_in_count < a.bcap ? *a.far_in_count : a.bcap;
-    const uint32_t nb = gridDim.x - a.ml_blocks, b0 = blockIdx.x - a.ml_blocks;
-    const uint32_t CH = bd * kFarEPT;
-    const uint32_t lane = tid & 31;
-    for (uint64_t base = (uint64_t)b0 * CH; base < nfar; base += (uint64_t)nb * CH) {
-      uint64_t ent[kFarEPT];
-#pragma unroll
-      for (int k = 0; k < kFarEPT; ++k) {
-        const uint64_t e = base + tid + (uint64_t)k * bd;
-        ent[k] = e < nfar ? a.far_in[e] : ~0ull;
-        if (e < nfar) {
-          const uint32_t q = (uint32_t)(ent[k] >> 32) & 0x1fffffffu;
-          const uint32_t t = q >> a.log_s;
-          if (t < a.ntiles_w) atomicAdd(&s_cnt[t], 1u);
-        }
-      }
-      __syncthreads();
-      reserve_tiles(a, s_cnt, s_base);
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < kFarEPT; ++k) {
-        const uint64_t e = base + tid + (uint64_t)k * bd;
-        bool app = false;
-        uint32_t slotb = 0;
-        uint64_t nent = 0;
-        if (e < nfar) {
-          const uint32_t p = (uint32_t)ent[k];
-          const uint32_t hi = (uint32_t)(ent[k] >> 32);
-          const uint32_t q = hi & 0x1fffffffu;
-          const uint32_t s = hi >> 29;
-          const uint32_t t = q >> a.log_s;
-          if (t < a.ntiles_w) {
-            const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
-            if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = q & smask;
-            // next hit: k or k+1 waves ahead in the paper's sense (Lemma 2)
-            const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
-            uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
-            while (d * a.WS > q2) --d;
-            while ((d + 1) * a.WS <= q2) ++d;
-            const uint64_t tgt = a.wave + d;
-            if (tgt < a.nwaves) {
-              app = true;
-              slotb = (uint32_t)(tgt % a.ring);
-              nent = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * a.WS) | (((s + 1) & 7) << 29)) << 32);
-            }
-          }
-        }
-        const uint32_t part = __ballot_sync(kFull, app);
-        if (app) {
-          const uint32_t grp = __match_any_sync(part, slotb);
-          const uint32_t leader = __ffs(grp) - 1;
-          uint32_t b = 0;
-          if (lane == leader) b = atomicAdd(&a.bcount[slotb], (uint32_t)__popc(grp));
-          b = __shfl_sync(grp, b, leader);
-          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
-          if (pos < a.bcap) a.buckets[(uint64_t)slotb * a.bcap + pos] = nent;
-          else atomicExch(a.overflow, 1);
-        }
-      }
-      __syncthreads();
-      for (uint32_t t = tid; t < a.ntiles_w; t += bd) s_cnt[t] = 0;
-      __syncthreads();
-    }
-  }
+  scatter_pass<true>(a, s_cnt, s_base, s_cum);
 }
 
 // ---------------------------------------------------------------------------
@@ -689,18 +680,17 @@ __global__ void k_bounds(const uint32_t* __restrict__ p, const uint64_t* __restr
   out[i] = lo;
 }
 
-// ---- large-prime setup: first hits, ML array, initial far buckets ---------
+// ---- large-prime setup: first hits -> ML state, initial far buckets ------
 struct SetupArgs {
   const uint32_t* primes;
   uint64_t i0, i_ml_end, i_end;  // ML = [i0, i_ml_end), far = [i_ml_end, i_end)
   uint64_t x0;                   // 2*g0 + 1
-  uint64_t* ml;
-  uint64_t* buckets;
-  uint32_t* bcount;
+  uint64_t* ml_state;
+  uint4* far_buckets;
+  uint32_t* far_bcount;
   uint32_t ring, bcap;
-  uint64_t nwaves;
-  uint32_t WS;
-  double inv_ws;
+  uint64_t nepochs;
+  uint64_t ES;
   int* overflow;
 };
 
@@ -709,23 +699,22 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   bool app = false;
   uint32_t slotb = 0;
-  uint64_t nent = 0;
+  uint4 ne = make_uint4(0, 0, 0, 0);
   if (i < a.i_end) {
     const uint32_t p = a.primes[i];
     uint32_t s;
-    // cofactor >= 2 (-> >= 7 after the wheel): never marks p itself, keeps
-    // the first hit within 3.5p of the interval start in overlap runs.
+    // cofactor >= 2 (-> >= 7 after the wheel): never marks p itself and
+    // keeps the first hit within 3.5p of the interval start in overlap runs
     const uint64_t pos = first_hit(p, ~0ull / p, a.x0, 2, s);
     if (i < a.i_ml_end) {
-      a.ml[i - a.i0] = (uint64_t)(uint32_t)pos | ((uint64_t)(p | (s << 29)) << 32);
+      a.ml_state[i - a.i0] = pos | ((uint64_t)s << 61);
     } else {
-      uint64_t d = (uint64_t)((double)pos * a.inv_ws);
-      while (d * a.WS > pos) --d;
-      while ((d + 1) * a.WS <= pos) ++d;
-      if (d < a.nwaves) {
+      const uint64_t d = pos / a.ES;
+      if (d < a.nepochs) {
         app = true;
         slotb = (uint32_t)(d % a.ring);
-        nent = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
+        const uint64_t qn = pos - d * a.ES;
+        ne = make_uint4(p, s, (uint32_t)qn, (uint32_t)(qn >> 32));
       }
     }
   }
@@ -734,10 +723,10 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
     const uint32_t grp = __match_any_sync(part, slotb);
     const uint32_t leader = __ffs(grp) - 1;
     uint32_t b = 0;
-    if (lane == leader) b = atomicAdd(&a.bcount[slotb], (uint32_t)__popc(grp));
+    if (lane == leader) b = atomicAdd(&a.far_bcount[slotb], (uint32_t)__popc(grp));
     b = __shfl_sync(grp, b, leader);
     const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
-    if (pos < a.bcap) a.buckets[(uint64_t)slotb * a.bcap + pos] = nent;
+    if (pos < a.bcap) a.far_buckets[(uint64_t)slotb * a.bcap + pos] = ne;
     else atomicExch(a.overflow, 1);
   }
 }

@@ -8,7 +8,8 @@ from oracle.oracle import Reference, Restated
 R = Reference(); O = Restated()
 ctx = E.context(0)
 cases = [(10, 2048, 4, False), (12, 4096, 8, False), (4, 2048, 4, True), (10, 6, 1, False), (16, 3, 5, True),
-         (13, 100, 300, True), (17, 9000, 64, False), (20, 523776, 16, False), (18, 2**30, 40, False)]
+         (13, 100, 300, True), (17, 9000, 64, False), (20, 523776, 16, False), (18, 2**30, 40, False),
+         (12, 2**40, 1000, False), (16, 2**45, 200, False), (13, 2**46 + 12345, 3001, False), (20, 2**41, 600, False)]
 ok = True
 for l, f, n, tm in cases:
     p = E.validate_params(l, f, n, test_mode=tm)
