@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "liberato_gpu.so")
+SO_PATH = os.environ.get("ERATO_GPU_SO") or os.path.join(_PKG, "liberato_gpu.so")
 
 u8p = C.POINTER(C.c_uint8)
 u64p = C.POINTER(C.c_uint64)

@@ -34,16 +34,16 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    so = SO.replace(".so", "_debug.so") if debug else SO
+    if not force and not debug and up_to_date():
         return SO
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", SO, *SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DEG_DEBUG"] if debug else []), "-o", so, *SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(SO)
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

@@ -208,6 +208,8 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(eg::ScatterSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure(8192 * 16));
@@ -279,8 +281,6 @@ struct Plan {
   uint64_t f, n, u, v, T, g0;
   uint32_t log_s, S, W, WS;
   uint64_t ntiles, nwaves;
-  uint32_t E;  // waves per epoch
-  uint64_t ES, nepochs;
   bool overlap;
 };
 
@@ -317,23 +317,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile, eg::kTileThreads, smem));
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
-    W = std::min<uint64_t>(W, eg::kMaxEpochTiles);
+    W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
+    // ML state / far entries keep positions in 29 bits: 3.5 * W * S < 2^29
+    W = std::min<uint64_t>(W, ((uint64_t)1 << 30) / (7ull * P.S));
     W = std::min<uint64_t>(W, P.ntiles);
     P.W = (uint32_t)std::max<uint64_t>(W, 1);
   }
   P.WS = P.W * P.S;
   P.nwaves = (P.ntiles + P.W - 1) / P.W;
-  // epochs: E waves share one large-prime scatter; ES < 2^32 - 2^28 and at
-  // most kMaxEpochTiles tiles (the scatter's shared-memory counters)
-  {
-    const uint64_t es_max = (1ull << 32) - (1ull << 28);
-    uint64_t E = std::max<uint64_t>(1, es_max / P.WS);
-    E = std::min<uint64_t>(E, eg::kMaxEpochTiles / P.W);
-    E = std::min<uint64_t>(E, P.nwaves);
-    P.E = (uint32_t)std::max<uint64_t>(E, 1);
-    P.ES = (uint64_t)P.E * P.WS;
-    P.nepochs = (P.nwaves + P.E - 1) / P.E;
-  }
 
   uint32_t launches = 0;
   for (int attempt = 0;; ++attempt) {
@@ -378,7 +369,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
     }
     // ---------------- 3. class boundaries (one host sync) ----------------
-    uint64_t thr[5] = {61, (uint64_t)P.S / 64, P.S, P.ES, std::max<uint64_t>(P.ES / 512, P.S)};
+    uint64_t thr[5] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(std::min<uint64_t>(P.WS / 16, 1u << 24), P.S)};
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
     eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 5, d_scal + 8);
     ++launches;
@@ -401,7 +392,6 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
                                                                          2 * P.g0 + 1, P.log_s, c->med.as<uint4>());
     ++launches;
     const bool have_large = nml + nfar > 0;
-    const uint64_t ntiles_e = std::min<uint64_t>((uint64_t)P.E * P.W, P.ntiles);
     uint32_t ring = 1, bcap = 1, hcap = 4;
     if (have_large) {
       const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
@@ -409,17 +399,17 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       const double eh = (double)P.S * (8.0 / 15.0) * sum_recip;
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
-      CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
-      CUDA_TRY(c->hits.ensure(ntiles_e * hcap * 4));
-      CUDA_TRY(c->hitcnt.ensure(ntiles_e * 4));
-      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, ntiles_e * 4, st));
+      CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 4));
+      CUDA_TRY(c->hits.ensure((uint64_t)P.W * hcap * 4));
+      CUDA_TRY(c->hitcnt.ensure((uint64_t)P.W * 4));
+      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
       if (nfar) {
-        ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.ES + 3, P.nepochs + 2);
-        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.ES))) + 0.01;
-        const double eb = (double)P.ES * (8.0 / 15.0) * sr_far;
+        ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.WS + 3, P.nwaves + 2);
+        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.WS))) + 0.01;
+        const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
         bcap = (uint32_t)std::min<double>((eb * 1.10 + 8192) * c->bcap_scale, (double)nfar + 64);
       }
-      CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 16));
+      CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 8));
       CUDA_TRY(c->bcount.ensure((uint64_t)ring * 4 + 4));
       CUDA_TRY(cudaMemsetAsync(c->bcount.p, 0, (uint64_t)ring * 4 + 4, st));
       CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));  // overflow flag
@@ -429,13 +419,13 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sa.i_ml_end = iWS;
       sa.i_end = nprimes;
       sa.x0 = 2 * P.g0 + 1;
-      sa.ml_state = c->ml.as<uint64_t>();
-      sa.far_buckets = c->buckets.as<uint4>();
+      sa.ml_state = c->ml.as<uint32_t>();
+      sa.far_buckets = c->buckets.as<uint64_t>();
       sa.far_bcount = c->bcount.as<uint32_t>();
       sa.ring = ring;
       sa.bcap = bcap;
-      sa.nepochs = P.nepochs;
-      sa.ES = P.ES;
+      sa.nwaves = P.nwaves;
+      sa.WS = P.WS;
       sa.overflow = reinterpret_cast<int*>(d_scal + 17);
       const uint64_t nl = nprimes - iS;
       eg::k_setup_large<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(sa);
@@ -465,24 +455,27 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     eg::ScatterArgs sc{};
     if (have_large) {
       sc.ml_p = c->primes.as<uint32_t>() + iS;
-      sc.ml_state = c->ml.as<uint64_t>();
+      sc.ml_state = c->ml.as<uint32_t>();
       sc.nml = (uint32_t)nml;
       sc.ndense = (uint32_t)std::min<uint64_t>(idense - iS, nml);
-      sc.far_buckets = c->buckets.as<uint4>();
+      {
+        const uint32_t bound = 8 * ((P.W + 1 + 14) / 15);  // admissible hits of a dense prime per wave
+        sc.dense_per_unit = std::max<uint32_t>(1, 512 / bound);
+      }
+      sc.far_buckets = c->buckets.as<uint64_t>();
       sc.far_bcount = c->bcount.as<uint32_t>();
       sc.ring = ring;
       sc.bcap = bcap;
-      sc.nepochs = P.nepochs;
-      sc.ES = P.ES;
+      sc.nwaves = P.nwaves;
+      sc.WS = P.WS;
       sc.log_s = P.log_s;
       sc.hits = c->hits.as<uint32_t>();
       sc.hitcnt = c->hitcnt.as<uint32_t>();
       sc.hcap = hcap;
       sc.overflow = reinterpret_cast<int*>(d_scal + 17);
     }
-    const uint32_t scatter_blocks = (uint32_t)c->nsm * 2;
     const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
-    const size_t nev = timing ? (size_t)(P.nwaves + P.nepochs) * 2 : 0;
+    const size_t nev = timing ? (size_t)P.nwaves * 4 : 0;
     while (c->phase_ev.size() < nev) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
@@ -490,44 +483,34 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     }
     size_t evi = 0;
     std::vector<std::pair<size_t, bool>> ev_pairs;  // (first event index, is_scatter)
-    for (uint64_t ep = 0; ep < P.nepochs; ++ep) {
-      const uint64_t w0 = ep * P.E, w1 = std::min<uint64_t>(w0 + P.E, P.nwaves);
-      const uint64_t etile0 = w0 * P.W;
-      const uint32_t nte = (uint32_t)std::min<uint64_t>((uint64_t)P.E * P.W, P.ntiles - etile0);
+    for (uint64_t w = 0; w < P.nwaves; ++w) {
+      const uint64_t tile0 = w * P.W;
+      const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
       if (have_large) {
-        sc.epoch = ep;
-        sc.ntiles_e = nte;
-        const uint32_t slot = nfar ? (uint32_t)(ep % ring) : 0;
-        sc.far_in = nfar ? c->buckets.as<uint4>() + (uint64_t)slot * bcap : nullptr;
+        sc.wave = w;
+        sc.ntiles_w = ntw;
+        const uint32_t slot = nfar ? (uint32_t)(w % ring) : 0;
+        sc.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         sc.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        eg::k_scatter<<<scatter_blocks, eg::kScatterThreads, 0, st>>>(sc);
+        eg::k_scatter<<<c->nsm, eg::kScatterThreads, sizeof(eg::ScatterSmem), st>>>(sc);
         if (timing) {
           CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           ev_pairs.push_back({evi, true});
           evi += 2;
         }
         ++launches;
+        ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
-      for (uint64_t w = w0; w < w1; ++w) {
-        const uint64_t tile0 = w * P.W;
-        const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
-        ta.tile0 = tile0;
-        if (have_large) {
-          ta.hits = c->hits.as<uint32_t>() + (tile0 - etile0) * hcap;
-          ta.hitcnt = c->hitcnt.as<uint32_t>() + (tile0 - etile0);
-          // the far bucket consumed by this epoch's scatter is reset by its last wave
-          ta.reset_bucket_count = (nfar && w + 1 == w1) ? c->bcount.as<uint32_t>() + (ep % ring) : nullptr;
-        }
-        if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        launch_tiles(c, st, ta, ntw);
-        if (timing) {
-          CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
-          ev_pairs.push_back({evi, false});
-          evi += 2;
-        }
-        ++launches;
+      ta.tile0 = tile0;
+      if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
+      launch_tiles(c, st, ta, ntw);
+      if (timing) {
+        CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
+        ev_pairs.push_back({evi, false});
+        evi += 2;
       }
+      ++launches;
     }
     CUDA_TRY(cudaGetLastError());
     if (dev_count) CUDA_TRY(cudaMemcpyAsync(dev_count, d_count, 8, cudaMemcpyDeviceToDevice, st));

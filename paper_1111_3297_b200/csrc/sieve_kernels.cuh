@@ -23,6 +23,25 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// EG_CHECK: device-side bounds checks, compiled in with -DEG_DEBUG (debug
+// builds only; compute-sanitizer is unavailable on the GPU pool).
+#ifdef EG_DEBUG
+#include <cstdio>
+#define EG_CHECK(cond, ...)                                            \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      printf("EG_CHECK failed %s:%d: %s | ", __FILE__, __LINE__, #cond); \
+      printf(__VA_ARGS__);                                             \
+      printf("\n");                                                    \
+      __trap();                                                        \
+    }                                                                  \
+  } while (0)
+#else
+#define EG_CHECK(cond, ...) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace eg {
 
 constexpr uint32_t kFull = 0xffffffffu;
@@ -324,6 +343,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     const uint4* h4 = reinterpret_cast<const uint4*>(h);
     for (uint32_t i = tid; i < n4; i += bd) {
       const uint4 v = h4[i];
+      EG_CHECK(v.x < S && v.y < S && v.z < S && v.w < S, "hit record out of tile %u %u %u %u", v.x, v.y, v.z, v.w);
       mark(tile, v.x);
       mark(tile, v.y);
       mark(tile, v.z);
@@ -377,168 +397,278 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Large primes (p > S).  The interval is cut into EPOCHS of E waves
-// (ES = E*W*S bits, ES < 2^32).  Once per epoch the scatter kernel walks
-// every large prime through the epoch and emits one 32-bit hit record (the
-// offset inside the tile) per wheel-admissible multiple into the list of
-// the tile it falls in; the tile kernels of the epoch's waves then consume
-// those lists.  This is the paper's bucket sort (large_kernel.hpp: each
-// (p,q) entry lands in the bucket of the segment it hits and the segment
-// consumes its bucket) with the bucket contents materialised as hit records,
-// because ~148 tiles are sieved at once and a prime below E*W*S hits many
-// of them.
-//   ML  (S < p <= ES): per-prime state, u64 = q | s << 61 (q = index offset
-//       of the next hit from the current epoch start), visited every epoch.
-//       dense ML (p <= ES/512) is walked warp-per-prime: lane j follows
-//       wheel class (s+j)&7 of period j>>3, so a warp's 32 lanes sit in
-//       ~60 different tiles and the smem counters see no contention.
-//   far (p > ES): at most one hit per epoch; bucketed by the epoch of its
-//       next hit (ring of epoch buckets, 16-byte entries {p | s<<32, q}).
-// Emission is a per-CTA counting sort: pass 1 counts hits per tile in
-// shared memory, one global atomicAdd per (CTA, tile) reserves a contiguous
-// slot range, pass 2 re-walks and writes.
+// Large primes (p > S), one scatter launch per wave of W tiles (WS = W*S
+// bits).  The paper's bucket sort (large_kernel.hpp: each (p,q) entry lands
+// in the bucket of the segment it next hits and that segment consumes it)
+// rebuilt for ~148 tiles in flight: the scatter walks every large prime with
+// a hit in the wave and emits one record per wheel-admissible multiple into
+// the list of the tile it falls in; the tile kernel then consumes its list.
+//   ML  (S < p <= WS, several hits per wave): state per prime, u32
+//       pos | s << 29 (pos = index offset of the next hit from the current
+//       wave start), visited every wave.  dense ML (many hits) is walked
+//       warp-per-prime (lane j: wheel class (s+j)&7, period j>>3), sparse
+//       ML lane-per-prime with whole wheel periods unrolled.
+//   far (p > WS, at most one hit per wave): u64 entries p | (q | s<<29)<<32
+//       in a ring of per-wave buckets; after its hit an entry is re-bucketed
+//       into the wave of its next hit.
+// Every record passes through shared memory: per round each warp takes one
+// work unit, the CTA counts records per tile (and per target bucket), scans,
+// reserves one contiguous global range per tile with one atomicAdd, places
+// the records sorted by tile in a staging buffer and flushes them with
+// coalesced stores — no scattered 4-byte writes reach L2.
 struct ScatterArgs {
-  const uint32_t* ml_p;  // ML primes (ascending)
-  uint64_t* ml_state;    // q | s << 61
+  const uint32_t* ml_p;  // ML primes, ascending
+  uint32_t* ml_state;    // pos | s << 29
   uint32_t nml, ndense;  // the first ndense ML primes are dense
-  const uint4* far_in;   // this epoch's far bucket
+  uint32_t dense_per_unit;
+  const uint64_t* far_in;  // bucket of this wave
   const uint32_t* far_in_count;
-  uint4* far_buckets;  // [ring][bcap]
+  uint64_t* far_buckets;  // [ring][bcap]
   uint32_t* far_bcount;
   uint32_t ring, bcap;
-  uint64_t epoch, nepochs;
-  uint64_t ES;          // epoch span in bits (< 2^32)
-  uint32_t ntiles_e;    // tiles in this epoch (<= kMaxEpochTiles)
+  uint64_t wave, nwaves;
+  uint32_t WS;        // wave span in bits
+  uint32_t ntiles_w;  // tiles in this wave
   uint32_t log_s;
-  uint32_t* hits;       // [ntiles_e][hcap]
-  uint32_t* hitcnt;     // [ntiles_e]
+  uint32_t* hits;     // [ntiles_w][hcap]
+  uint32_t* hitcnt;   // [ntiles_w]
   uint32_t hcap;
   int* overflow;
 };
 
-constexpr int kScatterThreads = 512;
+constexpr int kScatterThreads = 1024;
 constexpr int kScatterWarps = kScatterThreads / 32;
-constexpr int kMaxEpochTiles = 4096;
+constexpr int kMaxWaveTiles = 1024;
+constexpr int kStageRecs = 16384;  // >= 32 warps x 512 records per unit
+constexpr int kMaxRing = 64;       // far re-bucketing staged when ring <= kMaxRing
+constexpr int kFarStage = kScatterWarps * 32;
 
-template <bool kWrite>
-__device__ __forceinline__ void emit(const ScatterArgs& a, uint32_t* s_cnt, const uint32_t* s_base, uint64_t pos) {
-  const uint32_t t = (uint32_t)(pos >> a.log_s);
-  if (t < a.ntiles_e) {
-    if (!kWrite) {
-      atomicAdd(&s_cnt[t], 1u);
-    } else {
-      const uint32_t slot = s_base[t] + atomicAdd(&s_cnt[t], 1u);
-      if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = (uint32_t)pos & ((1u << a.log_s) - 1);
+struct ScatterSmem {
+  uint32_t cnt[kMaxWaveTiles];
+  uint32_t off[kMaxWaveTiles];
+  uint32_t base[kMaxWaveTiles];
+  uint32_t stage[kStageRecs];
+  uint32_t fcnt[kMaxRing];
+  uint32_t foff[kMaxRing];
+  uint32_t fbase[kMaxRing];
+  uint64_t fstage[kFarStage];
+  uint32_t cum[8];
+  uint32_t total;
+  uint32_t ftotal;
+};
+
+// kPass 0: count records per tile; kPass 1: place them into the stage
+template <int kPass>
+__device__ __forceinline__ void put(ScatterSmem& sm, const ScatterArgs& a, uint32_t pos) {
+  const uint32_t t = pos >> a.log_s;
+  if (t < a.ntiles_w) {
+    const uint32_t k = atomicAdd(&sm.cnt[t], 1u);
+    if (kPass == 1) {
+      EG_CHECK(sm.off[t] + k < kStageRecs, "stage t=%u off=%u k=%u", t, sm.off[t], k);
+      sm.stage[sm.off[t] + k] = pos;
     }
   }
 }
 
-// One pass over this CTA's share of the epoch's large primes.
-template <bool kWrite>
-__device__ void scatter_pass(const ScatterArgs& a, uint32_t* s_cnt, const uint32_t* s_base, const uint32_t* s_cum) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t gw = (uint64_t)blockIdx.x * kScatterWarps + (threadIdx.x >> 5);
-  const uint64_t nw = (uint64_t)gridDim.x * kScatterWarps;
-  const uint64_t ES = a.ES;
-  // dense ML: warp per prime
-  for (uint64_t i = gw; i < a.ndense; i += nw) {
-    const uint32_t p = a.ml_p[i];
-    const uint64_t st = a.ml_state[i];
-    const uint64_t q0 = st & ((1ull << 61) - 1);
-    const uint32_t s0 = (uint32_t)(st >> 61);
-    uint64_t pos = q0 + (uint64_t)p * (nib(s_cum[s0], lane & 7) + 15u * (lane >> 3));
-    const uint64_t step = 60ull * p;
-    for (; pos < ES; pos += step) emit<kWrite>(a, s_cnt, s_base, pos);
-    if (kWrite) {
-      // next hit = the smallest lane exit; its lane gives the class
-      const uint32_t ex = (uint32_t)(pos - ES);  // < 60p: fits u32 for dense primes
-      const uint32_t m = __reduce_min_sync(kFull, ex);
-      const uint32_t who = __ffs(__ballot_sync(kFull, ex == m)) - 1;
-      if (lane == 0) a.ml_state[i] = (uint64_t)m | ((uint64_t)((s0 + who) & 7) << 61);
-    }
+template <int kPass>
+__device__ __forceinline__ void put4(ScatterSmem& sm, const ScatterArgs& a, uint32_t p0, uint32_t p1, uint32_t p2,
+                                     uint32_t p3) {
+  const uint32_t n = a.ntiles_w, ls = a.log_s;
+  const uint32_t t0 = p0 >> ls, t1 = p1 >> ls, t2 = p2 >> ls, t3 = p3 >> ls;
+  uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
+  if (t0 < n) k0 = atomicAdd(&sm.cnt[t0], 1u);
+  if (t1 < n) k1 = atomicAdd(&sm.cnt[t1], 1u);
+  if (t2 < n) k2 = atomicAdd(&sm.cnt[t2], 1u);
+  if (t3 < n) k3 = atomicAdd(&sm.cnt[t3], 1u);
+  if (kPass == 1) {
+    EG_CHECK((t0 >= n || sm.off[t0] + k0 < kStageRecs) && (t1 >= n || sm.off[t1] + k1 < kStageRecs) &&
+                 (t2 >= n || sm.off[t2] + k2 < kStageRecs) && (t3 >= n || sm.off[t3] + k3 < kStageRecs),
+             "stage4");
+    if (t0 < n) sm.stage[sm.off[t0] + k0] = p0;
+    if (t1 < n) sm.stage[sm.off[t1] + k1] = p1;
+    if (t2 < n) sm.stage[sm.off[t2] + k2] = p2;
+    if (t3 < n) sm.stage[sm.off[t3] + k3] = p3;
   }
-  // sparse ML: lane per prime
-  const uint64_t nsp = a.nml - a.ndense;
-  for (uint64_t b = gw * 32; b < nsp; b += nw * 32) {
-    const uint64_t i = a.ndense + b + lane;
+}
+
+// Walk one work unit (uniform per warp).  unit < ud: dense; < ud+us: sparse;
+// else far.
+template <int kPass>
+__device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
+                          uint32_t nfar) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t WS = a.WS;
+  if (unit < ud) {
+    const uint64_t i0 = unit * a.dense_per_unit;
+    for (uint32_t k = 0; k < a.dense_per_unit; ++k) {
+      const uint64_t i = i0 + k;
+      if (i >= a.ndense) break;
+      const uint32_t p = a.ml_p[i];
+      const uint32_t st = a.ml_state[i];
+      const uint32_t s0 = st >> 29;
+      uint32_t pos = (st & 0x1fffffffu) + p * (nib(sm.cum[s0], lane & 7) + 15u * (lane >> 3));
+      const uint32_t step = 60u * p;
+      for (; pos + 3 * step < WS; pos += 4 * step) put4<kPass>(sm, a, pos, pos + step, pos + 2 * step, pos + 3 * step);
+      for (; pos < WS; pos += step) put<kPass>(sm, a, pos);
+      if (kPass == 1) {
+        const uint32_t ex = pos - WS;  // next hit of this lane's progression
+        const uint32_t m = __reduce_min_sync(kFull, ex);
+        const uint32_t who = __ffs(__ballot_sync(kFull, ex == m)) - 1;
+        if (lane == 0) a.ml_state[i] = m | (((s0 + who) & 7) << 29);
+      }
+    }
+  } else if (unit < ud + us) {
+    const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
     if (i < a.nml) {
       const uint32_t p = a.ml_p[i];
-      const uint64_t st = a.ml_state[i];
-      uint64_t pos = st & ((1ull << 61) - 1);
-      uint32_t s = (uint32_t)(st >> 61);
-      while (pos < ES) {
-        emit<kWrite>(a, s_cnt, s_base, pos);
-        pos += (uint64_t)wheel_D(s) * p;
-        s = (s + 1) & 7;
+      const uint32_t st = a.ml_state[i];
+      uint32_t pos = st & 0x1fffffffu;
+      const uint32_t s = st >> 29;
+      const uint32_t cp = sm.cum[s];
+      const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
+                     o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
+      const uint32_t per = 15u * p;
+      for (; pos + o7 < WS; pos += per) {
+        put4<kPass>(sm, a, pos, pos + o1, pos + o2, pos + o3);
+        put4<kPass>(sm, a, pos + o4, pos + o5, pos + o6, pos + o7);
       }
-      if (kWrite) a.ml_state[i] = (pos - ES) | ((uint64_t)s << 61);
+      const uint32_t offs[8] = {0, o1, o2, o3, o4, o5, o6, o7};
+      uint32_t k = 0;
+#pragma unroll
+      for (int j = 0; j < 7; ++j)
+        if (pos + offs[j] < WS) {
+          put<kPass>(sm, a, pos + offs[j]);
+          k = j + 1;
+        }
+      if (kPass == 1) {
+        uint32_t nxt = pos;
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+          if ((uint32_t)j == k) nxt = pos + offs[j];
+        a.ml_state[i] = (nxt - WS) | (((s + k) & 7) << 29);
+      }
     }
-  }
-  // far: one hit, then re-bucket into the epoch of the next hit
-  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  for (uint64_t b = gw * 32; b < nfar; b += nw * 32) {
-    const uint64_t i = b + lane;
-    bool app = false;
-    uint32_t slotb = 0;
-    uint4 ne = make_uint4(0, 0, 0, 0);
+  } else {
+    const uint64_t i = (unit - ud - us) * 32 + lane;
     if (i < nfar) {
-      const uint4 e = a.far_in[i];
-      const uint32_t p = e.x, s = e.y;
-      const uint64_t q = (uint64_t)e.z | ((uint64_t)e.w << 32);
-      emit<kWrite>(a, s_cnt, s_base, q);
-      if (kWrite) {
-        const uint64_t q2 = q + (uint64_t)wheel_D(s) * p;
-        const uint64_t d = q2 / ES;
-        const uint64_t tgt = a.epoch + d;
-        if (tgt < a.nepochs) {
-          app = true;
-          slotb = (uint32_t)(tgt % a.ring);
-          const uint64_t qn = q2 - d * ES;
-          ne = make_uint4(p, (s + 1) & 7, (uint32_t)qn, (uint32_t)(qn >> 32));
+      const uint64_t e = a.far_in[i];
+      const uint32_t p = (uint32_t)e;
+      const uint32_t hi = (uint32_t)(e >> 32);
+      const uint32_t q = hi & 0x1fffffffu, s = hi >> 29;
+      put<kPass>(sm, a, q);
+      // next hit k or k+1 waves ahead (Lemma 2)
+      const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
+      const uint64_t d = q2 / WS;
+      const uint64_t tgt = a.wave + d;
+      if (tgt < a.nwaves) {
+        const uint32_t slot = (uint32_t)(tgt % a.ring);
+        const uint64_t ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
+        if (a.ring <= kMaxRing) {
+          const uint32_t k = atomicAdd(&sm.fcnt[slot], 1u);
+          if (kPass == 1) sm.fstage[sm.foff[slot] + k] = ne;
+        } else if (kPass == 1) {  // large rings: direct warp-aggregated append
+          const uint32_t grp = __match_any_sync(__activemask(), slot);
+          const uint32_t leader = __ffs(grp) - 1;
+          uint32_t b = 0;
+          if (lane == leader) b = atomicAdd(&a.far_bcount[slot], (uint32_t)__popc(grp));
+          b = __shfl_sync(grp, b, leader);
+          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
+          if (pos < a.bcap) a.far_buckets[(uint64_t)slot * a.bcap + pos] = ne;
+          else atomicExch(a.overflow, 1);
         }
       }
     }
-    if (kWrite) {
-      const uint32_t part = __ballot_sync(kFull, app);
-      if (app) {
-        const uint32_t grp = __match_any_sync(part, slotb);
-        const uint32_t leader = __ffs(grp) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&a.far_bcount[slotb], (uint32_t)__popc(grp));
-        base = __shfl_sync(grp, base, leader);
-        const uint32_t pos = base + __popc(grp & ((1u << lane) - 1));
-        if (pos < a.bcap) a.far_buckets[(uint64_t)slotb * a.bcap + pos] = ne;
-        else atomicExch(a.overflow, 1);
-      }
-    }
   }
 }
 
-__global__ void __launch_bounds__(kScatterThreads) k_scatter(const ScatterArgs a) {
-  __shared__ uint32_t s_cnt[kMaxEpochTiles];
-  __shared__ uint32_t s_base[kMaxEpochTiles];
-  __shared__ uint32_t s_cum[8];
-  const uint32_t tid = threadIdx.x;
-  for (uint32_t t = tid; t < a.ntiles_e; t += blockDim.x) s_cnt[t] = 0;
+// exclusive scan of n (<= 1024) counters by one warp; reserves global ranges
+__device__ __forceinline__ uint32_t scan_reserve(uint32_t* cnt, uint32_t* off, uint32_t* base, uint32_t n,
+                                                 uint32_t* gcount, uint32_t cap, int* overflow) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t run = 0;
+  for (uint32_t t0 = 0; t0 < n; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    const uint32_t c = t < n ? cnt[t] : 0;
+    uint32_t x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (t < n) {
+      off[t] = run + x - c;
+      if (c) {
+        const uint32_t b = atomicAdd(&gcount[t], c);
+        base[t] = b;
+        if (b + c > cap) atomicExch(overflow, 1);
+      }
+      cnt[t] = 0;
+    }
+    run += __shfl_sync(kFull, x, 31);
+  }
+  return run;
+}
+
+__global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nt = a.ntiles_w;
+  const uint32_t nring = a.ring <= kMaxRing ? a.ring : 0;
+  for (uint32_t t = tid; t < nt; t += blockDim.x) sm.cnt[t] = 0;
+  if (tid < kMaxRing) sm.fcnt[tid] = 0;
   if (tid < 8) {
     uint32_t v = 0;
     for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
-    s_cum[tid] = v;
+    sm.cum[tid] = v;
   }
+  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
+  const uint64_t ud = (a.ndense + a.dense_per_unit - 1) / a.dense_per_unit;
+  const uint64_t us = (a.nml - a.ndense + 31) / 32;
+  const uint64_t uf = (nfar + 31) / 32;
+  const uint64_t units = ud + us + uf;
+  const uint64_t G = gridDim.x;
   __syncthreads();
-  scatter_pass<false>(a, s_cnt, s_base, s_cum);
-  __syncthreads();
-  for (uint32_t t = tid; t < a.ntiles_e; t += blockDim.x) {
-    const uint32_t c = s_cnt[t];
-    if (c) {
-      const uint32_t b = atomicAdd(&a.hitcnt[t], c);
-      s_base[t] = b;
-      if (b + c > a.hcap) atomicExch(a.overflow, 1);
+  for (uint64_t r0 = (uint64_t)blockIdx.x * kScatterWarps; r0 < units; r0 += G * kScatterWarps) {
+    const uint64_t unit = r0 + warp;
+    const bool has = unit < units;
+    // count
+    if (has) walk_unit<0>(sm, a, unit, ud, us, nfar);
+    __syncthreads();
+    // scan the counts into stage offsets; reserve global ranges
+    if (warp == 0) {
+      const uint32_t tot = scan_reserve(sm.cnt, sm.off, sm.base, nt, a.hitcnt, a.hcap, a.overflow);
+      if (lane == 0) sm.total = tot;
+    } else if (warp == 1) {
+      const uint32_t tot = nring ? scan_reserve(sm.fcnt, sm.foff, sm.fbase, nring, a.far_bcount, a.bcap, a.overflow) : 0;
+      if (lane == 0) sm.ftotal = tot;
     }
-    s_cnt[t] = 0;
+    __syncthreads();
+    EG_CHECK(sm.total <= kStageRecs && sm.ftotal <= kFarStage, "total=%u ftotal=%u", sm.total, sm.ftotal);
+    // place
+    if (has) walk_unit<1>(sm, a, unit, ud, us, nfar);
+    __syncthreads();
+    // the counters are free again (pass 1 left the placed counts in them)
+    for (uint32_t t = tid; t < nt; t += blockDim.x) sm.cnt[t] = 0;
+    if (tid < kMaxRing) sm.fcnt[tid] = 0;
+    // flush: consecutive stage slots of one tile go to consecutive addresses
+    const uint32_t total = sm.total, smask = (1u << a.log_s) - 1;
+    for (uint32_t i = tid; i < total; i += blockDim.x) {
+      const uint32_t pos = sm.stage[i];
+      const uint32_t t = pos >> a.log_s;
+      const uint32_t slot = sm.base[t] + (i - sm.off[t]);
+      EG_CHECK(t < nt && i >= sm.off[t], "flush t=%u nt=%u i=%u off=%u", t, nt, i, sm.off[t]);
+      if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = pos & smask;
+    }
+    const uint32_t ft = sm.ftotal;
+    for (uint32_t i = tid; i < ft; i += blockDim.x) {
+      // recover the slot from the stage position (nring <= 64: linear search)
+      uint32_t sl = 0;
+      while (sl + 1 < nring && sm.foff[sl + 1] <= i) ++sl;
+      const uint32_t pos = sm.fbase[sl] + (i - sm.foff[sl]);
+      if (pos < a.bcap) a.far_buckets[(uint64_t)sl * a.bcap + pos] = sm.fstage[i];
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  scatter_pass<true>(a, s_cnt, s_base, s_cum);
 }
 
 // ---------------------------------------------------------------------------
@@ -685,12 +815,12 @@ struct SetupArgs {
   const uint32_t* primes;
   uint64_t i0, i_ml_end, i_end;  // ML = [i0, i_ml_end), far = [i_ml_end, i_end)
   uint64_t x0;                   // 2*g0 + 1
-  uint64_t* ml_state;
-  uint4* far_buckets;
+  uint32_t* ml_state;
+  uint64_t* far_buckets;
   uint32_t* far_bcount;
   uint32_t ring, bcap;
-  uint64_t nepochs;
-  uint64_t ES;
+  uint64_t nwaves;
+  uint32_t WS;
   int* overflow;
 };
 
@@ -699,7 +829,7 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   bool app = false;
   uint32_t slotb = 0;
-  uint4 ne = make_uint4(0, 0, 0, 0);
+  uint64_t ne = 0;
   if (i < a.i_end) {
     const uint32_t p = a.primes[i];
     uint32_t s;
@@ -707,14 +837,13 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
     // keeps the first hit within 3.5p of the interval start in overlap runs
     const uint64_t pos = first_hit(p, ~0ull / p, a.x0, 2, s);
     if (i < a.i_ml_end) {
-      a.ml_state[i - a.i0] = pos | ((uint64_t)s << 61);
+      a.ml_state[i - a.i0] = (uint32_t)pos | (s << 29);
     } else {
-      const uint64_t d = pos / a.ES;
-      if (d < a.nepochs) {
+      const uint64_t d = pos / a.WS;
+      if (d < a.nwaves) {
         app = true;
         slotb = (uint32_t)(d % a.ring);
-        const uint64_t qn = pos - d * a.ES;
-        ne = make_uint4(p, s, (uint32_t)qn, (uint32_t)(qn >> 32));
+        ne = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
       }
     }
   }
