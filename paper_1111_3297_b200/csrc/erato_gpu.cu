@@ -318,6 +318,9 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
     W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
+    // the scatter stages <= 320 records per 4-prime octet unit: a prime above S
+    // hits <= 8*ceil((W+1)/15) <= 80 admissible multiples per wave for W <= 150
+    W = std::min<uint64_t>(W, 150);
     // ML state / far entries keep positions in 29 bits: 3.5 * W * S < 2^29
     W = std::min<uint64_t>(W, ((uint64_t)1 << 30) / (7ull * P.S));
     W = std::min<uint64_t>(W, P.ntiles);
@@ -369,7 +372,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
     }
     // ---------------- 3. class boundaries (one host sync) ----------------
-    uint64_t thr[5] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(std::min<uint64_t>(P.WS / 16, 1u << 24), P.S)};
+    uint64_t thr[5] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(P.WS / 8, P.S)};
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
     eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 5, d_scal + 8);
     ++launches;
@@ -458,10 +461,6 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sc.ml_state = c->ml.as<uint32_t>();
       sc.nml = (uint32_t)nml;
       sc.ndense = (uint32_t)std::min<uint64_t>(idense - iS, nml);
-      {
-        const uint32_t bound = 8 * ((P.W + 1 + 14) / 15);  // admissible hits of a dense prime per wave
-        sc.dense_per_unit = std::max<uint32_t>(1, 512 / bound);
-      }
       sc.far_buckets = c->buckets.as<uint64_t>();
       sc.far_bcount = c->bcount.as<uint32_t>();
       sc.ring = ring;

@@ -405,9 +405,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 // the list of the tile it falls in; the tile kernel then consumes its list.
 //   ML  (S < p <= WS, several hits per wave): state per prime, u32
 //       pos | s << 29 (pos = index offset of the next hit from the current
-//       wave start), visited every wave.  dense ML (many hits) is walked
-//       warp-per-prime (lane j: wheel class (s+j)&7, period j>>3), sparse
-//       ML lane-per-prime with whole wheel periods unrolled.
+//       wave start), visited every wave.  ML with p <= WS/8 is walked by
+//       8 lanes per prime (lane j: wheel class (s+j)&7, step 15p), the rest
+//       lane-per-prime (<= 8 hits per wave).
 //   far (p > WS, at most one hit per wave): u64 entries p | (q | s<<29)<<32
 //       in a ring of per-wave buckets; after its hit an entry is re-bucketed
 //       into the wave of its next hit.
@@ -420,7 +420,6 @@ struct ScatterArgs {
   const uint32_t* ml_p;  // ML primes, ascending
   uint32_t* ml_state;    // pos | s << 29
   uint32_t nml, ndense;  // the first ndense ML primes are dense
-  uint32_t dense_per_unit;
   const uint64_t* far_in;  // bucket of this wave
   const uint32_t* far_in_count;
   uint64_t* far_buckets;  // [ring][bcap]
@@ -439,9 +438,10 @@ struct ScatterArgs {
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterWarps = kScatterThreads / 32;
 constexpr int kMaxWaveTiles = 1024;
-constexpr int kStageRecs = 16384;  // >= 32 warps x 512 records per unit
+constexpr int kUnitsPerWarp = 2;
+constexpr int kStageRecs = kScatterWarps * kUnitsPerWarp * 320;  // a unit places <= 320 records
 constexpr int kMaxRing = 64;       // far re-bucketing staged when ring <= kMaxRing
-constexpr int kFarStage = kScatterWarps * 32;
+constexpr int kFarStage = kScatterWarps * kUnitsPerWarp * 32;
 
 struct ScatterSmem {
   uint32_t cnt[kMaxWaveTiles];
@@ -491,31 +491,39 @@ __device__ __forceinline__ void put4(ScatterSmem& sm, const ScatterArgs& a, uint
   }
 }
 
-// Walk one work unit (uniform per warp).  unit < ud: dense; < ud+us: sparse;
-// else far.
+// Walk one work unit (uniform per warp).  unit < ud: octet unit (4 ML
+// primes, 8 lanes each: lane j of an octet follows wheel class (s+j)&7 with
+// step 15p); < ud+us: 32 sparse ML primes, one per lane; else 32 far entries.
 template <int kPass>
 __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
                           uint32_t nfar) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t WS = a.WS;
   if (unit < ud) {
-    const uint64_t i0 = unit * a.dense_per_unit;
-    for (uint32_t k = 0; k < a.dense_per_unit; ++k) {
-      const uint64_t i = i0 + k;
-      if (i >= a.ndense) break;
-      const uint32_t p = a.ml_p[i];
-      const uint32_t st = a.ml_state[i];
-      const uint32_t s0 = st >> 29;
-      uint32_t pos = (st & 0x1fffffffu) + p * (nib(sm.cum[s0], lane & 7) + 15u * (lane >> 3));
-      const uint32_t step = 60u * p;
+    const uint64_t i = unit * 4 + (lane >> 3);
+    const uint32_t j = lane & 7;
+    const bool valid = i < a.ndense;
+    uint32_t p = 0, st = 0;
+    if (valid) {
+      p = a.ml_p[i];
+      st = a.ml_state[i];
+    }
+    const uint32_t s0 = st >> 29;
+    uint32_t pos = (st & 0x1fffffffu) + p * nib(sm.cum[s0], j);
+    const uint32_t step = 15u * p;
+    if (valid) {
       for (; pos + 3 * step < WS; pos += 4 * step) put4<kPass>(sm, a, pos, pos + step, pos + 2 * step, pos + 3 * step);
       for (; pos < WS; pos += step) put<kPass>(sm, a, pos);
-      if (kPass == 1) {
-        const uint32_t ex = pos - WS;  // next hit of this lane's progression
-        const uint32_t m = __reduce_min_sync(kFull, ex);
-        const uint32_t who = __ffs(__ballot_sync(kFull, ex == m)) - 1;
-        if (lane == 0) a.ml_state[i] = m | (((s0 + who) & 7) << 29);
-      }
+    }
+    if (kPass == 1) {
+      // next hit of the prime = smallest exit of its 8 class progressions
+      const uint32_t ex = pos - WS;
+      uint32_t m = ex;
+      m = min(m, __shfl_xor_sync(kFull, m, 1));
+      m = min(m, __shfl_xor_sync(kFull, m, 2));
+      m = min(m, __shfl_xor_sync(kFull, m, 4));
+      const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
+      if (valid && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
     }
   } else if (unit < ud + us) {
     const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
@@ -523,30 +531,13 @@ __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, 
       const uint32_t p = a.ml_p[i];
       const uint32_t st = a.ml_state[i];
       uint32_t pos = st & 0x1fffffffu;
-      const uint32_t s = st >> 29;
-      const uint32_t cp = sm.cum[s];
-      const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
-                     o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
-      const uint32_t per = 15u * p;
-      for (; pos + o7 < WS; pos += per) {
-        put4<kPass>(sm, a, pos, pos + o1, pos + o2, pos + o3);
-        put4<kPass>(sm, a, pos + o4, pos + o5, pos + o6, pos + o7);
+      uint32_t s = st >> 29;
+      while (pos < WS) {
+        put<kPass>(sm, a, pos);
+        pos += wheel_D(s) * p;
+        s = (s + 1) & 7;
       }
-      const uint32_t offs[8] = {0, o1, o2, o3, o4, o5, o6, o7};
-      uint32_t k = 0;
-#pragma unroll
-      for (int j = 0; j < 7; ++j)
-        if (pos + offs[j] < WS) {
-          put<kPass>(sm, a, pos + offs[j]);
-          k = j + 1;
-        }
-      if (kPass == 1) {
-        uint32_t nxt = pos;
-#pragma unroll
-        for (int j = 1; j < 8; ++j)
-          if ((uint32_t)j == k) nxt = pos + offs[j];
-        a.ml_state[i] = (nxt - WS) | (((s + k) & 7) << 29);
-      }
+      if (kPass == 1) a.ml_state[i] = (pos - WS) | (s << 29);
     }
   } else {
     const uint64_t i = (unit - ud - us) * 32 + lane;
@@ -622,17 +613,17 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArg
     sm.cum[tid] = v;
   }
   const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  const uint64_t ud = (a.ndense + a.dense_per_unit - 1) / a.dense_per_unit;
+  const uint64_t ud = (a.ndense + 3) / 4;
   const uint64_t us = (a.nml - a.ndense + 31) / 32;
   const uint64_t uf = (nfar + 31) / 32;
   const uint64_t units = ud + us + uf;
   const uint64_t G = gridDim.x;
   __syncthreads();
-  for (uint64_t r0 = (uint64_t)blockIdx.x * kScatterWarps; r0 < units; r0 += G * kScatterWarps) {
-    const uint64_t unit = r0 + warp;
-    const bool has = unit < units;
+  constexpr uint64_t kRound = (uint64_t)kScatterWarps * kUnitsPerWarp;
+  for (uint64_t r0 = (uint64_t)blockIdx.x * kRound; r0 < units; r0 += G * kRound) {
     // count
-    if (has) walk_unit<0>(sm, a, unit, ud, us, nfar);
+    for (int u = 0; u < kUnitsPerWarp; ++u)
+      if (r0 + warp + u * kScatterWarps < units) walk_unit<0>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar);
     __syncthreads();
     // scan the counts into stage offsets; reserve global ranges
     if (warp == 0) {
@@ -645,7 +636,8 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArg
     __syncthreads();
     EG_CHECK(sm.total <= kStageRecs && sm.ftotal <= kFarStage, "total=%u ftotal=%u", sm.total, sm.ftotal);
     // place
-    if (has) walk_unit<1>(sm, a, unit, ud, us, nfar);
+    for (int u = 0; u < kUnitsPerWarp; ++u)
+      if (r0 + warp + u * kScatterWarps < units) walk_unit<1>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar);
     __syncthreads();
     // the counters are free again (pass 1 left the placed counts in them)
     for (uint32_t t = tid; t < nt; t += blockDim.x) sm.cnt[t] = 0;
