@@ -437,18 +437,20 @@ struct ScatterArgs {
 
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterWarps = kScatterThreads / 32;
-constexpr int kMaxWaveTiles = 1024;
-constexpr int kUnitsPerWarp = 2;
+constexpr int kMaxWaveTiles = 256;
+constexpr int kUnitsPerWarp = 4;
 constexpr int kStageRecs = kScatterWarps * kUnitsPerWarp * 320;  // a unit places <= 320 records
 constexpr int kMaxRing = 64;       // far re-bucketing staged when ring <= kMaxRing
 constexpr int kFarStage = kScatterWarps * kUnitsPerWarp * 32;
 
 struct ScatterSmem {
-  uint32_t cnt[kMaxWaveTiles];
-  uint32_t off[kMaxWaveTiles];
-  uint32_t base[kMaxWaveTiles];
+  uint32_t cnt[kMaxWaveTiles];   // pass-0 counts
+  uint32_t cur[kMaxWaveTiles];   // pass-1 cursors
+  uint32_t off[kMaxWaveTiles];   // stage offsets (exclusive scan of cnt)
+  uint32_t base[kMaxWaveTiles];  // reserved global slot of the CTA's run
   uint32_t stage[kStageRecs];
   uint32_t fcnt[kMaxRing];
+  uint32_t fcur[kMaxRing];
   uint32_t foff[kMaxRing];
   uint32_t fbase[kMaxRing];
   uint64_t fstage[kFarStage];
@@ -462,7 +464,7 @@ template <int kPass>
 __device__ __forceinline__ void put(ScatterSmem& sm, const ScatterArgs& a, uint32_t pos) {
   const uint32_t t = pos >> a.log_s;
   if (t < a.ntiles_w) {
-    const uint32_t k = atomicAdd(&sm.cnt[t], 1u);
+    const uint32_t k = atomicAdd(kPass == 0 ? &sm.cnt[t] : &sm.cur[t], 1u);
     if (kPass == 1) {
       EG_CHECK(sm.off[t] + k < kStageRecs, "stage t=%u off=%u k=%u", t, sm.off[t], k);
       sm.stage[sm.off[t] + k] = pos;
@@ -476,10 +478,11 @@ __device__ __forceinline__ void put4(ScatterSmem& sm, const ScatterArgs& a, uint
   const uint32_t n = a.ntiles_w, ls = a.log_s;
   const uint32_t t0 = p0 >> ls, t1 = p1 >> ls, t2 = p2 >> ls, t3 = p3 >> ls;
   uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
-  if (t0 < n) k0 = atomicAdd(&sm.cnt[t0], 1u);
-  if (t1 < n) k1 = atomicAdd(&sm.cnt[t1], 1u);
-  if (t2 < n) k2 = atomicAdd(&sm.cnt[t2], 1u);
-  if (t3 < n) k3 = atomicAdd(&sm.cnt[t3], 1u);
+  uint32_t* const c = kPass == 0 ? sm.cnt : sm.cur;
+  if (t0 < n) k0 = atomicAdd(&c[t0], 1u);
+  if (t1 < n) k1 = atomicAdd(&c[t1], 1u);
+  if (t2 < n) k2 = atomicAdd(&c[t2], 1u);
+  if (t3 < n) k3 = atomicAdd(&c[t3], 1u);
   if (kPass == 1) {
     EG_CHECK((t0 >= n || sm.off[t0] + k0 < kStageRecs) && (t1 >= n || sm.off[t1] + k1 < kStageRecs) &&
                  (t2 >= n || sm.off[t2] + k2 < kStageRecs) && (t3 >= n || sm.off[t3] + k3 < kStageRecs),
@@ -491,23 +494,45 @@ __device__ __forceinline__ void put4(ScatterSmem& sm, const ScatterArgs& a, uint
   }
 }
 
-// Walk one work unit (uniform per warp).  unit < ud: octet unit (4 ML
-// primes, 8 lanes each: lane j of an octet follows wheel class (s+j)&7 with
-// step 15p); < ud+us: 32 sparse ML primes, one per lane; else 32 far entries.
+// Work units (uniform per warp).  unit < ud: octet unit (4 ML primes, 8
+// lanes each: lane j of an octet follows wheel class (s+j)&7 with step 15p);
+// < ud+us: 32 sparse ML primes, one per lane; else 32 far entries.  A unit's
+// data is loaded once per round (all units of a warp up front, so their
+// memory latencies overlap) and walked twice: pass 0 counts, pass 1 places.
+struct UnitData {
+  uint32_t x, y;  // ML: p, state ; far: entry lo, hi
+};
+
+__device__ __forceinline__ UnitData load_unit(const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
+                                              uint32_t nfar) {
+  const uint32_t lane = threadIdx.x & 31;
+  UnitData d{0, 0};
+  if (unit < ud) {
+    const uint64_t i = unit * 4 + (lane >> 3);
+    if (i < a.ndense) d = UnitData{a.ml_p[i], a.ml_state[i]};
+  } else if (unit < ud + us) {
+    const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
+    if (i < a.nml) d = UnitData{a.ml_p[i], a.ml_state[i]};
+  } else {
+    const uint64_t i = (unit - ud - us) * 32 + lane;
+    if (i < nfar) {
+      const uint64_t e = a.far_in[i];
+      d = UnitData{(uint32_t)e, (uint32_t)(e >> 32)};
+    }
+  }
+  return d;
+}
+
 template <int kPass>
 __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
-                          uint32_t nfar) {
+                          uint32_t nfar, const UnitData d) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t WS = a.WS;
   if (unit < ud) {
     const uint64_t i = unit * 4 + (lane >> 3);
     const uint32_t j = lane & 7;
     const bool valid = i < a.ndense;
-    uint32_t p = 0, st = 0;
-    if (valid) {
-      p = a.ml_p[i];
-      st = a.ml_state[i];
-    }
+    const uint32_t p = d.x, st = d.y;
     const uint32_t s0 = st >> 29;
     uint32_t pos = (st & 0x1fffffffu) + p * nib(sm.cum[s0], j);
     const uint32_t step = 15u * p;
@@ -528,10 +553,9 @@ __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, 
   } else if (unit < ud + us) {
     const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
     if (i < a.nml) {
-      const uint32_t p = a.ml_p[i];
-      const uint32_t st = a.ml_state[i];
-      uint32_t pos = st & 0x1fffffffu;
-      uint32_t s = st >> 29;
+      const uint32_t p = d.x;
+      uint32_t pos = d.y & 0x1fffffffu;
+      uint32_t s = d.y >> 29;
       while (pos < WS) {
         put<kPass>(sm, a, pos);
         pos += wheel_D(s) * p;
@@ -542,20 +566,18 @@ __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, 
   } else {
     const uint64_t i = (unit - ud - us) * 32 + lane;
     if (i < nfar) {
-      const uint64_t e = a.far_in[i];
-      const uint32_t p = (uint32_t)e;
-      const uint32_t hi = (uint32_t)(e >> 32);
-      const uint32_t q = hi & 0x1fffffffu, s = hi >> 29;
+      const uint32_t p = d.x;
+      const uint32_t q = d.y & 0x1fffffffu, s = d.y >> 29;
       put<kPass>(sm, a, q);
       // next hit k or k+1 waves ahead (Lemma 2)
       const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
-      const uint64_t d = q2 / WS;
-      const uint64_t tgt = a.wave + d;
+      const uint64_t dw = q2 / WS;
+      const uint64_t tgt = a.wave + dw;
       if (tgt < a.nwaves) {
         const uint32_t slot = (uint32_t)(tgt % a.ring);
-        const uint64_t ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
+        const uint64_t ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - dw * WS) | (((s + 1) & 7) << 29)) << 32);
         if (a.ring <= kMaxRing) {
-          const uint32_t k = atomicAdd(&sm.fcnt[slot], 1u);
+          const uint32_t k = atomicAdd(kPass == 0 ? &sm.fcnt[slot] : &sm.fcur[slot], 1u);
           if (kPass == 1) sm.fstage[sm.foff[slot] + k] = ne;
         } else if (kPass == 1) {  // large rings: direct warp-aggregated append
           const uint32_t grp = __match_any_sync(__activemask(), slot);
@@ -572,9 +594,8 @@ __device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, 
   }
 }
 
-// exclusive scan of n (<= 1024) counters by one warp; reserves global ranges
-__device__ __forceinline__ uint32_t scan_reserve(uint32_t* cnt, uint32_t* off, uint32_t* base, uint32_t n,
-                                                 uint32_t* gcount, uint32_t cap, int* overflow) {
+// exclusive scan of n (<= kMaxWaveTiles) counters by one warp
+__device__ __forceinline__ uint32_t warp_scan_off(const uint32_t* cnt, uint32_t* off, uint32_t n) {
   const uint32_t lane = threadIdx.x & 31;
   uint32_t run = 0;
   for (uint32_t t0 = 0; t0 < n; t0 += 32) {
@@ -585,15 +606,7 @@ __device__ __forceinline__ uint32_t scan_reserve(uint32_t* cnt, uint32_t* off, u
       const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
-    if (t < n) {
-      off[t] = run + x - c;
-      if (c) {
-        const uint32_t b = atomicAdd(&gcount[t], c);
-        base[t] = b;
-        if (b + c > cap) atomicExch(overflow, 1);
-      }
-      cnt[t] = 0;
-    }
+    if (t < n) off[t] = run + x - c;
     run += __shfl_sync(kFull, x, 31);
   }
   return run;
@@ -605,8 +618,14 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArg
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nt = a.ntiles_w;
   const uint32_t nring = a.ring <= kMaxRing ? a.ring : 0;
-  for (uint32_t t = tid; t < nt; t += blockDim.x) sm.cnt[t] = 0;
-  if (tid < kMaxRing) sm.fcnt[tid] = 0;
+  for (uint32_t t = tid; t < kMaxWaveTiles; t += blockDim.x) {
+    sm.cnt[t] = 0;
+    sm.cur[t] = 0;
+  }
+  if (tid < kMaxRing) {
+    sm.fcnt[tid] = 0;
+    sm.fcur[tid] = 0;
+  }
   if (tid < 8) {
     uint32_t v = 0;
     for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
@@ -618,30 +637,61 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArg
   const uint64_t uf = (nfar + 31) / 32;
   const uint64_t units = ud + us + uf;
   const uint64_t G = gridDim.x;
+  // tile t's global reservation is issued by thread kResv + t (warps 2..), tile
+  // slot t of the far ring by thread kResvF + t
+  constexpr uint32_t kResv = 64, kResvF = kResv + kMaxWaveTiles;
   __syncthreads();
   constexpr uint64_t kRound = (uint64_t)kScatterWarps * kUnitsPerWarp;
   for (uint64_t r0 = (uint64_t)blockIdx.x * kRound; r0 < units; r0 += G * kRound) {
-    // count
+    UnitData ud_[kUnitsPerWarp];
+#pragma unroll
     for (int u = 0; u < kUnitsPerWarp; ++u)
-      if (r0 + warp + u * kScatterWarps < units) walk_unit<0>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar);
+      ud_[u] = load_unit(a, r0 + warp + u * kScatterWarps, ud, us, nfar);
+    // pass 0: count records per tile (and per far target slot)
+#pragma unroll
+    for (int u = 0; u < kUnitsPerWarp; ++u)
+      if (r0 + warp + u * kScatterWarps < units)
+        walk_unit<0>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar, ud_[u]);
     __syncthreads();
-    // scan the counts into stage offsets; reserve global ranges
+    // stage offsets (warps 0/1); global reservations issued now, consumed after pass 1
+    uint32_t resv = 0, rc = 0;
     if (warp == 0) {
-      const uint32_t tot = scan_reserve(sm.cnt, sm.off, sm.base, nt, a.hitcnt, a.hcap, a.overflow);
+      const uint32_t tot = warp_scan_off(sm.cnt, sm.off, nt);
       if (lane == 0) sm.total = tot;
     } else if (warp == 1) {
-      const uint32_t tot = nring ? scan_reserve(sm.fcnt, sm.foff, sm.fbase, nring, a.far_bcount, a.bcap, a.overflow) : 0;
+      const uint32_t tot = nring ? warp_scan_off(sm.fcnt, sm.foff, nring) : 0;
       if (lane == 0) sm.ftotal = tot;
+    } else if (tid >= kResv && tid < kResv + nt) {
+      rc = sm.cnt[tid - kResv];
+      if (rc) resv = atomicAdd(&a.hitcnt[tid - kResv], rc);
+    } else if (tid >= kResvF && tid < kResvF + nring) {
+      rc = sm.fcnt[tid - kResvF];
+      if (rc) resv = atomicAdd(&a.far_bcount[tid - kResvF], rc);
+    }
+    __syncthreads();
+    // pass 1: place records into the stage, sorted by tile
+#pragma unroll
+    for (int u = 0; u < kUnitsPerWarp; ++u)
+      if (r0 + warp + u * kScatterWarps < units)
+        walk_unit<1>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar, ud_[u]);
+    if (tid >= kResv && tid < kResv + nt) {
+      sm.base[tid - kResv] = resv;
+      if (rc && resv + rc > a.hcap) atomicExch(a.overflow, 1);
+    } else if (tid >= kResvF && tid < kResvF + nring) {
+      sm.fbase[tid - kResvF] = resv;
+      if (rc && resv + rc > a.bcap) atomicExch(a.overflow, 1);
     }
     __syncthreads();
     EG_CHECK(sm.total <= kStageRecs && sm.ftotal <= kFarStage, "total=%u ftotal=%u", sm.total, sm.ftotal);
-    // place
-    for (int u = 0; u < kUnitsPerWarp; ++u)
-      if (r0 + warp + u * kScatterWarps < units) walk_unit<1>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar);
-    __syncthreads();
-    // the counters are free again (pass 1 left the placed counts in them)
-    for (uint32_t t = tid; t < nt; t += blockDim.x) sm.cnt[t] = 0;
-    if (tid < kMaxRing) sm.fcnt[tid] = 0;
+    // counters are free again
+    for (uint32_t t = tid; t < nt; t += blockDim.x) {
+      sm.cnt[t] = 0;
+      sm.cur[t] = 0;
+    }
+    if (tid < kMaxRing) {
+      sm.fcnt[tid] = 0;
+      sm.fcur[tid] = 0;
+    }
     // flush: consecutive stage slots of one tile go to consecutive addresses
     const uint32_t total = sm.total, smask = (1u << a.log_s) - 1;
     for (uint32_t i = tid; i < total; i += blockDim.x) {
