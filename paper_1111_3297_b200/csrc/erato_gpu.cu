@@ -84,6 +84,7 @@ uint64_t pi_upper(uint64_t x) {
 }
 
 constexpr uint32_t kBaseLogTile = 20;  // tile size for the sieve of [1, sqrt(v)]
+constexpr uint32_t kGenBlocksPerSm = 2;
 
 }  // namespace
 
@@ -96,6 +97,7 @@ struct erato_gpu_ctx {
   std::vector<uint32_t> h_sp;
   // grow-only run buffers
   DevBuf base_bits, primes, med, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
+  DevBuf recs, rcount, frecs, fslot, fcount;  // k_gen -> k_bin per-warp regions
   double hcap_scale = 1.0, bcap_scale = 1.0;
   cudaEvent_t ev[4] = {};
   std::vector<cudaEvent_t> phase_ev;  // pairs, grown on demand
@@ -208,8 +210,8 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8)));
-  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(eg::ScatterSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(eg::BinSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure(8192 * 16));
@@ -236,7 +238,7 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
-                    &c->outbuf})
+                    &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount})
     b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -318,9 +320,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
     W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
-    // the scatter stages <= 320 records per 4-prime octet unit: a prime above S
-    // hits <= 8*ceil((W+1)/15) <= 80 admissible multiples per wave for W <= 150
-    W = std::min<uint64_t>(W, 150);
+
     // ML state / far entries keep positions in 29 bits: 3.5 * W * S < 2^29
     W = std::min<uint64_t>(W, ((uint64_t)1 << 30) / (7ull * P.S));
     W = std::min<uint64_t>(W, P.ntiles);
@@ -395,7 +395,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
                                                                          2 * P.g0 + 1, P.log_s, c->med.as<uint4>());
     ++launches;
     const bool have_large = nml + nfar > 0;
-    uint32_t ring = 1, bcap = 1, hcap = 4;
+    uint32_t ring = 1, bcap = 1, hcap = 4, rcap = 1, fcap = 1;
     if (have_large) {
       const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
       const double sum_recip = std::max(0.0, std::log(lnP / std::log((double)P.S))) + 0.02;  // sum 1/p, S<p<=P
@@ -408,11 +408,24 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
       if (nfar) {
         ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.WS + 3, P.nwaves + 2);
+        if (ring > (uint32_t)eg::kMaxRing) return fail(ERATO_GPU_RANGE_TOO_LARGE, "far bucket ring exceeds 256 waves");
         const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.WS))) + 0.01;
         const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
         bcap = (uint32_t)std::min<double>((eb * 1.10 + 8192) * c->bcap_scale, (double)nfar + 64);
       }
       CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 8));
+      {
+        const uint64_t gen_warps = (uint64_t)c->nsm * kGenBlocksPerSm * (eg::kGenThreads / 32);
+        const double per_wave = eh * P.W;  // records per wave
+        rcap = (uint32_t)std::min<double>((per_wave / gen_warps * 1.3 + 2048) * c->hcap_scale, 1u << 30);
+        rcap = (rcap + 31) & ~31u;
+        fcap = nfar ? (uint32_t)std::min<double>(((double)bcap / gen_warps * 1.3 + 512) * c->bcap_scale, 1u << 30) : 1;
+        CUDA_TRY(c->recs.ensure(gen_warps * rcap * 4));
+        CUDA_TRY(c->rcount.ensure(gen_warps * 4));
+        CUDA_TRY(c->frecs.ensure(gen_warps * fcap * 8));
+        CUDA_TRY(c->fslot.ensure(gen_warps * fcap));
+        CUDA_TRY(c->fcount.ensure(gen_warps * 4));
+      }
       CUDA_TRY(c->bcount.ensure((uint64_t)ring * 4 + 4));
       CUDA_TRY(cudaMemsetAsync(c->bcount.p, 0, (uint64_t)ring * 4 + 4, st));
       CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));  // overflow flag
@@ -455,26 +468,48 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.table = static_cast<uint32_t*>(dev_table);
     ta.count = d_count;
     ta.p2_floor = P.overlap ? 1 : 0;
-    eg::ScatterArgs sc{};
+    const uint32_t gen_blocks = (uint32_t)c->nsm * kGenBlocksPerSm;
+    const uint32_t gen_warps = gen_blocks * (eg::kGenThreads / 32);
+    eg::GenArgs ga{};
+    eg::BinArgs ba{};
     if (have_large) {
-      sc.ml_p = c->primes.as<uint32_t>() + iS;
-      sc.ml_state = c->ml.as<uint32_t>();
-      sc.nml = (uint32_t)nml;
-      sc.ndense = (uint32_t)std::min<uint64_t>(idense - iS, nml);
-      sc.far_buckets = c->buckets.as<uint64_t>();
-      sc.far_bcount = c->bcount.as<uint32_t>();
-      sc.ring = ring;
-      sc.bcap = bcap;
-      sc.nwaves = P.nwaves;
-      sc.WS = P.WS;
-      sc.log_s = P.log_s;
-      sc.hits = c->hits.as<uint32_t>();
-      sc.hitcnt = c->hitcnt.as<uint32_t>();
-      sc.hcap = hcap;
-      sc.overflow = reinterpret_cast<int*>(d_scal + 17);
+      ga.ml_p = c->primes.as<uint32_t>() + iS;
+      ga.ml_state = c->ml.as<uint32_t>();
+      ga.nml = (uint32_t)nml;
+      ga.noct = (uint32_t)std::min<uint64_t>(idense - iS, nml);
+      ga.bcap = bcap;
+      ga.ring = ring;
+      ga.nwaves = P.nwaves;
+      ga.WS = P.WS;
+      ga.log_s = P.log_s;
+      ga.recs = c->recs.as<uint32_t>();
+      ga.rcount = c->rcount.as<uint32_t>();
+      ga.rcap = rcap;
+      ga.frecs = c->frecs.as<uint64_t>();
+      ga.fslot = c->fslot.as<uint8_t>();
+      ga.fcount = c->fcount.as<uint32_t>();
+      ga.fcap = fcap;
+      ga.overflow = reinterpret_cast<int*>(d_scal + 17);
+      ba.recs = ga.recs;
+      ba.rcount = ga.rcount;
+      ba.rcap = rcap;
+      ba.nregions = gen_warps;
+      ba.frecs = nfar ? ga.frecs : nullptr;
+      ba.fslot = ga.fslot;
+      ba.fcount = ga.fcount;
+      ba.fcap = fcap;
+      ba.log_s = P.log_s;
+      ba.hits = c->hits.as<uint32_t>();
+      ba.hitcnt = c->hitcnt.as<uint32_t>();
+      ba.hcap = hcap;
+      ba.far_buckets = c->buckets.as<uint64_t>();
+      ba.far_bcount = c->bcount.as<uint32_t>();
+      ba.ring = ring;
+      ba.bcap = bcap;
+      ba.overflow = ga.overflow;
     }
     const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
-    const size_t nev = timing ? (size_t)P.nwaves * 4 : 0;
+    const size_t nev = timing ? (size_t)P.nwaves * 6 : 0;
     while (c->phase_ev.size() < nev) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
@@ -486,19 +521,21 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       const uint64_t tile0 = w * P.W;
       const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
       if (have_large) {
-        sc.wave = w;
-        sc.ntiles_w = ntw;
+        ga.wave = w;
+        ga.ntiles_w = ntw;
+        ba.ntiles_w = ntw;
         const uint32_t slot = nfar ? (uint32_t)(w % ring) : 0;
-        sc.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
-        sc.far_in_count = c->bcount.as<uint32_t>() + slot;
+        ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
+        ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        eg::k_scatter<<<c->nsm, eg::kScatterThreads, sizeof(eg::ScatterSmem), st>>>(sc);
+        eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
+        eg::k_bin<<<(uint32_t)c->nsm * 3, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
         if (timing) {
           CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           ev_pairs.push_back({evi, true});
           evi += 2;
         }
-        ++launches;
+        launches += 2;
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
       ta.tile0 = tile0;

@@ -397,205 +397,198 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Large primes (p > S), one scatter launch per wave of W tiles (WS = W*S
-// bits).  The paper's bucket sort (large_kernel.hpp: each (p,q) entry lands
-// in the bucket of the segment it next hits and that segment consumes it)
-// rebuilt for ~148 tiles in flight: the scatter walks every large prime with
-// a hit in the wave and emits one record per wheel-admissible multiple into
-// the list of the tile it falls in; the tile kernel then consumes its list.
-//   ML  (S < p <= WS, several hits per wave): state per prime, u32
-//       pos | s << 29 (pos = index offset of the next hit from the current
-//       wave start), visited every wave.  ML with p <= WS/8 is walked by
-//       8 lanes per prime (lane j: wheel class (s+j)&7, step 15p), the rest
-//       lane-per-prime (<= 8 hits per wave).
-//   far (p > WS, at most one hit per wave): u64 entries p | (q | s<<29)<<32
-//       in a ring of per-wave buckets; after its hit an entry is re-bucketed
-//       into the wave of its next hit.
-// Every record passes through shared memory: per round each warp takes one
-// work unit, the CTA counts records per tile (and per target bucket), scans,
-// reserves one contiguous global range per tile with one atomicAdd, places
-// the records sorted by tile in a staging buffer and flushes them with
-// coalesced stores — no scattered 4-byte writes reach L2.
-struct ScatterArgs {
+// Large primes (p > S), per wave of W tiles (WS = W*S bits).  The paper's
+// bucket sort (large_kernel.hpp: an entry lands in the bucket of the segment
+// it next hits, the segment consumes the bucket, the entry advances and
+// re-buckets) rebuilt for ~148 tiles in flight, in two kernels per wave:
+//
+//  k_gen  walks every large prime with a hit in the wave — ML primes
+//         (S < p <= WS: state u32 pos | s << 29, visited every wave) and the
+//         wave's far bucket (p > WS, u64 entries p | (q | s<<29) << 32) —
+//         and appends one record per wheel-admissible multiple (its position
+//         in the wave) to a per-warp region of a global buffer, 32 lanes at a
+//         time (ballot/popc compaction: coalesced stores, no atomics).  Far
+//         entries leave re-bucketed into per-warp regions tagged with the
+//         ring slot of the wave of their next hit (Lemma 2).
+//         Control flow is warp-uniform (loops run while any lane has work).
+//  k_bin  counting-sorts the records by tile (and the re-bucketed far entries
+//         by ring slot) in shared memory, chunk by chunk, and flushes each
+//         tile's run with coalesced stores into that tile's hit list; one
+//         global atomicAdd per (chunk, tile) reserves the run.
+//
+// ML primes with p <= WS/8 are walked by 8 lanes (lane j of an octet: wheel
+// class (s+j)&7, step 15p), the others one per lane.
+struct GenArgs {
   const uint32_t* ml_p;  // ML primes, ascending
   uint32_t* ml_state;    // pos | s << 29
-  uint32_t nml, ndense;  // the first ndense ML primes are dense
-  const uint64_t* far_in;  // bucket of this wave
+  uint32_t nml, noct;    // the first noct ML primes are walked by octets
+  const uint64_t* far_in;  // far bucket of this wave
   const uint32_t* far_in_count;
-  uint64_t* far_buckets;  // [ring][bcap]
-  uint32_t* far_bcount;
-  uint32_t ring, bcap;
+  uint32_t bcap, ring;
   uint64_t wave, nwaves;
   uint32_t WS;        // wave span in bits
-  uint32_t ntiles_w;  // tiles in this wave
+  uint32_t ntiles_w;  // tiles in this wave (records beyond are dropped)
   uint32_t log_s;
-  uint32_t* hits;     // [ntiles_w][hcap]
-  uint32_t* hitcnt;   // [ntiles_w]
-  uint32_t hcap;
+  uint32_t* recs;     // [nwarps][rcap] records (position in the wave)
+  uint32_t* rcount;   // [nwarps]
+  uint32_t rcap;
+  uint64_t* frecs;    // [nwarps][fcap] re-bucketed far entries
+  uint8_t* fslot;     // [nwarps][fcap] their ring slot
+  uint32_t* fcount;   // [nwarps]
+  uint32_t fcap;
   int* overflow;
 };
 
-constexpr int kScatterThreads = 1024;
-constexpr int kScatterWarps = kScatterThreads / 32;
-constexpr int kMaxWaveTiles = 256;
-constexpr int kUnitsPerWarp = 4;
-constexpr int kStageRecs = kScatterWarps * kUnitsPerWarp * 320;  // a unit places <= 320 records
-constexpr int kMaxRing = 64;       // far re-bucketing staged when ring <= kMaxRing
-constexpr int kFarStage = kScatterWarps * kUnitsPerWarp * 32;
+constexpr int kGenThreads = 512;
 
-struct ScatterSmem {
-  uint32_t cnt[kMaxWaveTiles];   // pass-0 counts
-  uint32_t cur[kMaxWaveTiles];   // pass-1 cursors
-  uint32_t off[kMaxWaveTiles];   // stage offsets (exclusive scan of cnt)
-  uint32_t base[kMaxWaveTiles];  // reserved global slot of the CTA's run
-  uint32_t stage[kStageRecs];
-  uint32_t fcnt[kMaxRing];
-  uint32_t fcur[kMaxRing];
-  uint32_t foff[kMaxRing];
-  uint32_t fbase[kMaxRing];
-  uint64_t fstage[kFarStage];
-  uint32_t cum[8];
-  uint32_t total;
-  uint32_t ftotal;
+struct WarpOut {
+  uint32_t* rec;
+  uint32_t n, cap;
+  uint64_t* frec;
+  uint8_t* fsl;
+  uint32_t fn, fcap;
 };
 
-// kPass 0: count records per tile; kPass 1: place them into the stage
-template <int kPass>
-__device__ __forceinline__ void put(ScatterSmem& sm, const ScatterArgs& a, uint32_t pos) {
-  const uint32_t t = pos >> a.log_s;
-  if (t < a.ntiles_w) {
-    const uint32_t k = atomicAdd(kPass == 0 ? &sm.cnt[t] : &sm.cur[t], 1u);
-    if (kPass == 1) {
-      EG_CHECK(sm.off[t] + k < kStageRecs, "stage t=%u off=%u k=%u", t, sm.off[t], k);
-      sm.stage[sm.off[t] + k] = pos;
-    }
-  }
-}
-
-template <int kPass>
-__device__ __forceinline__ void put4(ScatterSmem& sm, const ScatterArgs& a, uint32_t p0, uint32_t p1, uint32_t p2,
-                                     uint32_t p3) {
-  const uint32_t n = a.ntiles_w, ls = a.log_s;
-  const uint32_t t0 = p0 >> ls, t1 = p1 >> ls, t2 = p2 >> ls, t3 = p3 >> ls;
-  uint32_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
-  uint32_t* const c = kPass == 0 ? sm.cnt : sm.cur;
-  if (t0 < n) k0 = atomicAdd(&c[t0], 1u);
-  if (t1 < n) k1 = atomicAdd(&c[t1], 1u);
-  if (t2 < n) k2 = atomicAdd(&c[t2], 1u);
-  if (t3 < n) k3 = atomicAdd(&c[t3], 1u);
-  if (kPass == 1) {
-    EG_CHECK((t0 >= n || sm.off[t0] + k0 < kStageRecs) && (t1 >= n || sm.off[t1] + k1 < kStageRecs) &&
-                 (t2 >= n || sm.off[t2] + k2 < kStageRecs) && (t3 >= n || sm.off[t3] + k3 < kStageRecs),
-             "stage4");
-    if (t0 < n) sm.stage[sm.off[t0] + k0] = p0;
-    if (t1 < n) sm.stage[sm.off[t1] + k1] = p1;
-    if (t2 < n) sm.stage[sm.off[t2] + k2] = p2;
-    if (t3 < n) sm.stage[sm.off[t3] + k3] = p3;
-  }
-}
-
-// Work units (uniform per warp).  unit < ud: octet unit (4 ML primes, 8
-// lanes each: lane j of an octet follows wheel class (s+j)&7 with step 15p);
-// < ud+us: 32 sparse ML primes, one per lane; else 32 far entries.  A unit's
-// data is loaded once per round (all units of a warp up front, so their
-// memory latencies overlap) and walked twice: pass 0 counts, pass 1 places.
-struct UnitData {
-  uint32_t x, y;  // ML: p, state ; far: entry lo, hi
-};
-
-__device__ __forceinline__ UnitData load_unit(const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
-                                              uint32_t nfar) {
+// append the valid lanes' records (warp-uniform call)
+__device__ __forceinline__ void wappend(WarpOut& o, bool valid, uint32_t rec) {
   const uint32_t lane = threadIdx.x & 31;
-  UnitData d{0, 0};
-  if (unit < ud) {
-    const uint64_t i = unit * 4 + (lane >> 3);
-    if (i < a.ndense) d = UnitData{a.ml_p[i], a.ml_state[i]};
-  } else if (unit < ud + us) {
-    const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
-    if (i < a.nml) d = UnitData{a.ml_p[i], a.ml_state[i]};
-  } else {
-    const uint64_t i = (unit - ud - us) * 32 + lane;
-    if (i < nfar) {
-      const uint64_t e = a.far_in[i];
-      d = UnitData{(uint32_t)e, (uint32_t)(e >> 32)};
-    }
-  }
-  return d;
+  const uint32_t m = __ballot_sync(kFull, valid);
+  const uint32_t k = o.n + __popc(m & ((1u << lane) - 1));
+  if (valid && k < o.cap) o.rec[k] = rec;
+  o.n += __popc(m);
 }
 
-template <int kPass>
-__device__ void walk_unit(ScatterSmem& sm, const ScatterArgs& a, uint64_t unit, uint64_t ud, uint64_t us,
-                          uint32_t nfar, const UnitData d) {
+__global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
+  __shared__ uint32_t s_cum[8];
+  if (threadIdx.x < 8) {
+    uint32_t v = 0;
+    for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[threadIdx.x][k] << (4 * k);
+    s_cum[threadIdx.x] = v;
+  }
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t)blockIdx.x * (kGenThreads / 32) + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * (kGenThreads / 32);
   const uint32_t WS = a.WS;
-  if (unit < ud) {
-    const uint64_t i = unit * 4 + (lane >> 3);
+  const uint32_t lim = a.ntiles_w << a.log_s;  // positions past the last tile of the wave are dropped
+  WarpOut o{a.recs + gw * a.rcap, 0, a.rcap, a.frecs + gw * a.fcap, a.fslot + gw * a.fcap, 0, a.fcap};
+
+  // octets: 4 primes per warp-step
+  const uint64_t uo = (a.noct + 3) / 4;
+  for (uint64_t u = gw; u < uo; u += nw) {
+    const uint64_t i = u * 4 + (lane >> 3);
     const uint32_t j = lane & 7;
-    const bool valid = i < a.ndense;
-    const uint32_t p = d.x, st = d.y;
+    const bool ok = i < a.noct;
+    const uint32_t p = ok ? a.ml_p[i] : 0;
+    const uint32_t st = ok ? a.ml_state[i] : 0;
     const uint32_t s0 = st >> 29;
-    uint32_t pos = (st & 0x1fffffffu) + p * nib(sm.cum[s0], j);
+    uint32_t pos = ok ? (st & 0x1fffffffu) + p * nib(s_cum[s0], j) : WS;
     const uint32_t step = 15u * p;
-    if (valid) {
-      for (; pos + 3 * step < WS; pos += 4 * step) put4<kPass>(sm, a, pos, pos + step, pos + 2 * step, pos + 3 * step);
-      for (; pos < WS; pos += step) put<kPass>(sm, a, pos);
+    while (__any_sync(kFull, pos < WS)) {
+      const bool v = pos < WS;
+      wappend(o, v && pos < lim, pos);
+      if (v) pos += step;
     }
-    if (kPass == 1) {
-      // next hit of the prime = smallest exit of its 8 class progressions
-      const uint32_t ex = pos - WS;
-      uint32_t m = ex;
-      m = min(m, __shfl_xor_sync(kFull, m, 1));
-      m = min(m, __shfl_xor_sync(kFull, m, 2));
-      m = min(m, __shfl_xor_sync(kFull, m, 4));
-      const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
-      if (valid && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
-    }
-  } else if (unit < ud + us) {
-    const uint64_t i = a.ndense + (unit - ud) * 32 + lane;
-    if (i < a.nml) {
-      const uint32_t p = d.x;
-      uint32_t pos = d.y & 0x1fffffffu;
-      uint32_t s = d.y >> 29;
-      while (pos < WS) {
-        put<kPass>(sm, a, pos);
+    // next hit of the prime = smallest exit of its 8 class progressions
+    const uint32_t ex = pos - WS;
+    uint32_t m = ex;
+    m = min(m, __shfl_xor_sync(kFull, m, 1));
+    m = min(m, __shfl_xor_sync(kFull, m, 2));
+    m = min(m, __shfl_xor_sync(kFull, m, 4));
+    const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
+    if (ok && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
+  }
+  // single ML primes: one per lane
+  const uint64_t us = (a.nml - a.noct + 31) / 32;
+  for (uint64_t u = gw; u < us; u += nw) {
+    const uint64_t i = a.noct + u * 32 + lane;
+    const bool ok = i < a.nml;
+    const uint32_t p = ok ? a.ml_p[i] : 0;
+    const uint32_t st = ok ? a.ml_state[i] : 0;
+    uint32_t pos = ok ? (st & 0x1fffffffu) : WS;
+    uint32_t s = st >> 29;
+    while (__any_sync(kFull, pos < WS)) {
+      const bool v = pos < WS;
+      wappend(o, v && pos < lim, pos);
+      if (v) {
         pos += wheel_D(s) * p;
         s = (s + 1) & 7;
       }
-      if (kPass == 1) a.ml_state[i] = (pos - WS) | (s << 29);
     }
-  } else {
-    const uint64_t i = (unit - ud - us) * 32 + lane;
-    if (i < nfar) {
-      const uint32_t p = d.x;
-      const uint32_t q = d.y & 0x1fffffffu, s = d.y >> 29;
-      put<kPass>(sm, a, q);
-      // next hit k or k+1 waves ahead (Lemma 2)
+    if (ok) a.ml_state[i] = (pos - WS) | (s << 29);
+  }
+  // far: exactly one hit in this wave, then re-bucket
+  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
+  const uint64_t uf = (nfar + 31) / 32;
+  for (uint64_t u = gw; u < uf; u += nw) {
+    const uint64_t i = u * 32 + lane;
+    const bool ok = i < nfar;
+    const uint64_t e = ok ? a.far_in[i] : 0;
+    const uint32_t p = (uint32_t)e;
+    const uint32_t q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
+    wappend(o, ok && q < lim, q);
+    bool keep = false;
+    uint32_t slot = 0;
+    uint64_t ne = 0;
+    if (ok) {
       const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
-      const uint64_t dw = q2 / WS;
-      const uint64_t tgt = a.wave + dw;
+      const uint64_t d = q2 / WS;
+      const uint64_t tgt = a.wave + d;
       if (tgt < a.nwaves) {
-        const uint32_t slot = (uint32_t)(tgt % a.ring);
-        const uint64_t ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - dw * WS) | (((s + 1) & 7) << 29)) << 32);
-        if (a.ring <= kMaxRing) {
-          const uint32_t k = atomicAdd(kPass == 0 ? &sm.fcnt[slot] : &sm.fcur[slot], 1u);
-          if (kPass == 1) sm.fstage[sm.foff[slot] + k] = ne;
-        } else if (kPass == 1) {  // large rings: direct warp-aggregated append
-          const uint32_t grp = __match_any_sync(__activemask(), slot);
-          const uint32_t leader = __ffs(grp) - 1;
-          uint32_t b = 0;
-          if (lane == leader) b = atomicAdd(&a.far_bcount[slot], (uint32_t)__popc(grp));
-          b = __shfl_sync(grp, b, leader);
-          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
-          if (pos < a.bcap) a.far_buckets[(uint64_t)slot * a.bcap + pos] = ne;
-          else atomicExch(a.overflow, 1);
-        }
+        keep = true;
+        slot = (uint32_t)(tgt % a.ring);
+        ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
       }
     }
+    const uint32_t m = __ballot_sync(kFull, keep);
+    const uint32_t k = o.fn + __popc(m & ((1u << lane) - 1));
+    if (keep && k < o.fcap) {
+      o.frec[k] = ne;
+      o.fsl[k] = (uint8_t)slot;
+    }
+    o.fn += __popc(m);
+  }
+  if (lane == 0) {
+    a.rcount[gw] = min(o.n, o.cap);
+    a.fcount[gw] = min(o.fn, o.fcap);
+    if (o.n > o.cap || o.fn > o.fcap) atomicExch(a.overflow, 1);
   }
 }
 
-// exclusive scan of n (<= kMaxWaveTiles) counters by one warp
-__device__ __forceinline__ uint32_t warp_scan_off(const uint32_t* cnt, uint32_t* off, uint32_t n) {
+struct BinArgs {
+  const uint32_t* recs;
+  const uint32_t* rcount;
+  uint32_t rcap, nregions;
+  const uint64_t* frecs;
+  const uint8_t* fslot;
+  const uint32_t* fcount;
+  uint32_t fcap;
+  uint32_t ntiles_w, log_s;
+  uint32_t* hits;    // [ntiles_w][hcap]
+  uint32_t* hitcnt;  // [ntiles_w]
+  uint32_t hcap;
+  uint64_t* far_buckets;  // [ring][bcap]
+  uint32_t* far_bcount;
+  uint32_t ring, bcap;
+  int* overflow;
+};
+
+constexpr int kBinThreads = 512;
+constexpr int kBinChunk = 8192;  // records per chunk
+constexpr int kMaxWaveTiles = 256;
+constexpr int kMaxRing = 256;
+
+struct BinSmem {
+  uint32_t a[kBinChunk];  // chunk as loaded
+  uint32_t b[kBinChunk];  // chunk sorted by tile
+  uint32_t cnt[kMaxWaveTiles];
+  uint32_t off[kMaxWaveTiles];
+  uint32_t base[kMaxWaveTiles];
+  uint32_t total;
+};
+
+__device__ __forceinline__ uint32_t block_excl_scan_small(const uint32_t* cnt, uint32_t* off, uint32_t n) {
+  // one warp scans n (<= 256) counters
   const uint32_t lane = threadIdx.x & 31;
   uint32_t run = 0;
   for (uint32_t t0 = 0; t0 < n; t0 += 32) {
@@ -612,104 +605,89 @@ __device__ __forceinline__ uint32_t warp_scan_off(const uint32_t* cnt, uint32_t*
   return run;
 }
 
-__global__ void __launch_bounds__(kScatterThreads, 1) k_scatter(const ScatterArgs a) {
-  extern __shared__ uint4 smem_raw[];
-  ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nt = a.ntiles_w;
-  const uint32_t nring = a.ring <= kMaxRing ? a.ring : 0;
-  for (uint32_t t = tid; t < kMaxWaveTiles; t += blockDim.x) {
-    sm.cnt[t] = 0;
-    sm.cur[t] = 0;
-  }
-  if (tid < kMaxRing) {
-    sm.fcnt[tid] = 0;
-    sm.fcur[tid] = 0;
-  }
-  if (tid < 8) {
-    uint32_t v = 0;
-    for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
-    sm.cum[tid] = v;
-  }
-  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  const uint64_t ud = (a.ndense + 3) / 4;
-  const uint64_t us = (a.nml - a.ndense + 31) / 32;
-  const uint64_t uf = (nfar + 31) / 32;
-  const uint64_t units = ud + us + uf;
-  const uint64_t G = gridDim.x;
-  // tile t's global reservation is issued by thread kResv + t (warps 2..), tile
-  // slot t of the far ring by thread kResvF + t
-  constexpr uint32_t kResv = 64, kResvF = kResv + kMaxWaveTiles;
+// Sort one chunk of `n` (<= kBinChunk) u32 keys already in sm.a by bucket
+// key >> shift (< nb buckets) into sm.b and flush each bucket's run to
+// dst[bucket * cap + reserved..] (value = key & vmask).
+__device__ void bin_chunk32(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask, uint32_t* dst,
+                            uint32_t* gcnt, uint32_t cap, int* overflow) {
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
-  constexpr uint64_t kRound = (uint64_t)kScatterWarps * kUnitsPerWarp;
-  for (uint64_t r0 = (uint64_t)blockIdx.x * kRound; r0 < units; r0 += G * kRound) {
-    UnitData ud_[kUnitsPerWarp];
-#pragma unroll
-    for (int u = 0; u < kUnitsPerWarp; ++u)
-      ud_[u] = load_unit(a, r0 + warp + u * kScatterWarps, ud, us, nfar);
-    // pass 0: count records per tile (and per far target slot)
-#pragma unroll
-    for (int u = 0; u < kUnitsPerWarp; ++u)
-      if (r0 + warp + u * kScatterWarps < units)
-        walk_unit<0>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar, ud_[u]);
-    __syncthreads();
-    // stage offsets (warps 0/1); global reservations issued now, consumed after pass 1
-    uint32_t resv = 0, rc = 0;
-    if (warp == 0) {
-      const uint32_t tot = warp_scan_off(sm.cnt, sm.off, nt);
-      if (lane == 0) sm.total = tot;
-    } else if (warp == 1) {
-      const uint32_t tot = nring ? warp_scan_off(sm.fcnt, sm.foff, nring) : 0;
-      if (lane == 0) sm.ftotal = tot;
-    } else if (tid >= kResv && tid < kResv + nt) {
-      rc = sm.cnt[tid - kResv];
-      if (rc) resv = atomicAdd(&a.hitcnt[tid - kResv], rc);
-    } else if (tid >= kResvF && tid < kResvF + nring) {
-      rc = sm.fcnt[tid - kResvF];
-      if (rc) resv = atomicAdd(&a.far_bcount[tid - kResvF], rc);
+  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.a[i] >> shift], 1u);
+  __syncthreads();
+  if (tid < 32) {
+    const uint32_t tot = block_excl_scan_small(sm.cnt, sm.off, nb);
+    if (tid == 0) sm.total = tot;
+  }
+  uint32_t resv = 0, rc = 0;
+  if (tid >= 32 && tid < 32 + nb) {  // reservations in flight during the placement
+    rc = sm.cnt[tid - 32];
+    if (rc) resv = atomicAdd(&gcnt[tid - 32], rc);
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t key = sm.a[i];
+    const uint32_t t = key >> shift;
+    sm.b[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
+  }
+  if (tid >= 32 && tid < 32 + nb) {
+    sm.base[tid - 32] = resv;
+    if (rc && resv + rc > cap) atomicExch(overflow, 1);
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t key = sm.b[i];
+    const uint32_t t = key >> shift;
+    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
+    EG_CHECK(t < nb && i >= sm.off[t], "bin t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
+    if (slot < cap) dst[(uint64_t)t * cap + slot] = key & vmask;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  BinSmem& sm = *reinterpret_cast<BinSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t smask = (1u << a.log_s) - 1;
+  // hit records: regions round-robin over the CTAs, chunk by chunk
+  for (uint32_t r = blockIdx.x; r < a.nregions; r += gridDim.x) {
+    const uint32_t cnt = a.rcount[r];
+    const uint32_t* src = a.recs + (uint64_t)r * a.rcap;
+    for (uint32_t c0 = 0; c0 < cnt; c0 += kBinChunk) {
+      const uint32_t n = min((uint32_t)kBinChunk, cnt - c0);
+      for (uint32_t i = tid; i < n; i += blockDim.x) sm.a[i] = src[c0 + i];
+      bin_chunk32(sm, n, a.log_s, a.ntiles_w, smask, a.hits, a.hitcnt, a.hcap, a.overflow);
     }
-    __syncthreads();
-    // pass 1: place records into the stage, sorted by tile
-#pragma unroll
-    for (int u = 0; u < kUnitsPerWarp; ++u)
-      if (r0 + warp + u * kScatterWarps < units)
-        walk_unit<1>(sm, a, r0 + warp + u * kScatterWarps, ud, us, nfar, ud_[u]);
-    if (tid >= kResv && tid < kResv + nt) {
-      sm.base[tid - kResv] = resv;
-      if (rc && resv + rc > a.hcap) atomicExch(a.overflow, 1);
-    } else if (tid >= kResvF && tid < kResvF + nring) {
-      sm.fbase[tid - kResvF] = resv;
-      if (rc && resv + rc > a.bcap) atomicExch(a.overflow, 1);
+  }
+  // re-bucketed far entries: runs per ring slot (kept simple: per-entry
+  // warp-aggregated append within each region, entries of one region are
+  // mostly a few slots)
+  if (a.frecs) {
+    const uint32_t lane = tid & 31;
+    for (uint32_t r = blockIdx.x; r < a.nregions; r += gridDim.x) {
+      const uint32_t cnt = a.fcount[r];
+      const uint64_t* fr = a.frecs + (uint64_t)r * a.fcap;
+      const uint8_t* fs = a.fslot + (uint64_t)r * a.fcap;
+      for (uint32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
+        const uint32_t i = i0 + tid;
+        const bool ok = i < cnt;
+        const uint32_t slot = ok ? fs[i] : 0xffffffffu;
+        const uint32_t part = __ballot_sync(kFull, ok);
+        if (ok) {
+          const uint32_t grp = __match_any_sync(part, slot);
+          const uint32_t leader = __ffs(grp) - 1;
+          uint32_t b = 0;
+          if (lane == leader) b = atomicAdd(&a.far_bcount[slot], (uint32_t)__popc(grp));
+          b = __shfl_sync(grp, b, leader);
+          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
+          if (pos < a.bcap) a.far_buckets[(uint64_t)slot * a.bcap + pos] = fr[i];
+          else atomicExch(a.overflow, 1);
+        }
+      }
     }
-    __syncthreads();
-    EG_CHECK(sm.total <= kStageRecs && sm.ftotal <= kFarStage, "total=%u ftotal=%u", sm.total, sm.ftotal);
-    // counters are free again
-    for (uint32_t t = tid; t < nt; t += blockDim.x) {
-      sm.cnt[t] = 0;
-      sm.cur[t] = 0;
-    }
-    if (tid < kMaxRing) {
-      sm.fcnt[tid] = 0;
-      sm.fcur[tid] = 0;
-    }
-    // flush: consecutive stage slots of one tile go to consecutive addresses
-    const uint32_t total = sm.total, smask = (1u << a.log_s) - 1;
-    for (uint32_t i = tid; i < total; i += blockDim.x) {
-      const uint32_t pos = sm.stage[i];
-      const uint32_t t = pos >> a.log_s;
-      const uint32_t slot = sm.base[t] + (i - sm.off[t]);
-      EG_CHECK(t < nt && i >= sm.off[t], "flush t=%u nt=%u i=%u off=%u", t, nt, i, sm.off[t]);
-      if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = pos & smask;
-    }
-    const uint32_t ft = sm.ftotal;
-    for (uint32_t i = tid; i < ft; i += blockDim.x) {
-      // recover the slot from the stage position (nring <= 64: linear search)
-      uint32_t sl = 0;
-      while (sl + 1 < nring && sm.foff[sl + 1] <= i) ++sl;
-      const uint32_t pos = sm.fbase[sl] + (i - sm.foff[sl]);
-      if (pos < a.bcap) a.far_buckets[(uint64_t)sl * a.bcap + pos] = sm.fstage[i];
-    }
-    __syncthreads();
   }
 }
 
