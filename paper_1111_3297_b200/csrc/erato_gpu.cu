@@ -470,6 +470,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.p2_floor = P.overlap ? 1 : 0;
     const uint32_t gen_blocks = (uint32_t)c->nsm * kGenBlocksPerSm;
     const uint32_t gen_warps = gen_blocks * (eg::kGenThreads / 32);
+    const uint32_t bin_blocks = std::max<uint32_t>((uint32_t)c->nsm * 2, (gen_warps + eg::kMaxRegionsPerCta - 1) / eg::kMaxRegionsPerCta);
     eg::GenArgs ga{};
     eg::BinArgs ba{};
     if (have_large) {
@@ -529,7 +530,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
         eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
-        eg::k_bin<<<(uint32_t)c->nsm * 3, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
+        eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
         if (timing) {
           CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           ev_pairs.push_back({evi, true});

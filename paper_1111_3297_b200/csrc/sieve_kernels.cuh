@@ -473,49 +473,73 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
   const uint32_t lim = a.ntiles_w << a.log_s;  // positions past the last tile of the wave are dropped
   WarpOut o{a.recs + gw * a.rcap, 0, a.rcap, a.frecs + gw * a.fcap, a.fslot + gw * a.fcap, 0, a.fcap};
 
-  // octets: 4 primes per warp-step
+  // octets: 4 primes per warp-step (next step's data prefetched)
   const uint64_t uo = (a.noct + 3) / 4;
-  for (uint64_t u = gw; u < uo; u += nw) {
-    const uint64_t i = u * 4 + (lane >> 3);
+  {
     const uint32_t j = lane & 7;
-    const bool ok = i < a.noct;
-    const uint32_t p = ok ? a.ml_p[i] : 0;
-    const uint32_t st = ok ? a.ml_state[i] : 0;
-    const uint32_t s0 = st >> 29;
-    uint32_t pos = ok ? (st & 0x1fffffffu) + p * nib(s_cum[s0], j) : WS;
-    const uint32_t step = 15u * p;
-    while (__any_sync(kFull, pos < WS)) {
-      const bool v = pos < WS;
-      wappend(o, v && pos < lim, pos);
-      if (v) pos += step;
+    uint64_t u = gw;
+    uint32_t pn = 0, stn = 0;
+    if (u < uo && u * 4 + (lane >> 3) < a.noct) {
+      pn = a.ml_p[u * 4 + (lane >> 3)];
+      stn = a.ml_state[u * 4 + (lane >> 3)];
     }
-    // next hit of the prime = smallest exit of its 8 class progressions
-    const uint32_t ex = pos - WS;
-    uint32_t m = ex;
-    m = min(m, __shfl_xor_sync(kFull, m, 1));
-    m = min(m, __shfl_xor_sync(kFull, m, 2));
-    m = min(m, __shfl_xor_sync(kFull, m, 4));
-    const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
-    if (ok && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
-  }
-  // single ML primes: one per lane
-  const uint64_t us = (a.nml - a.noct + 31) / 32;
-  for (uint64_t u = gw; u < us; u += nw) {
-    const uint64_t i = a.noct + u * 32 + lane;
-    const bool ok = i < a.nml;
-    const uint32_t p = ok ? a.ml_p[i] : 0;
-    const uint32_t st = ok ? a.ml_state[i] : 0;
-    uint32_t pos = ok ? (st & 0x1fffffffu) : WS;
-    uint32_t s = st >> 29;
-    while (__any_sync(kFull, pos < WS)) {
-      const bool v = pos < WS;
-      wappend(o, v && pos < lim, pos);
-      if (v) {
-        pos += wheel_D(s) * p;
-        s = (s + 1) & 7;
+    for (; u < uo; u += nw) {
+      const uint64_t i = u * 4 + (lane >> 3);
+      const bool ok = i < a.noct;
+      const uint32_t p = pn, st = stn;
+      const uint64_t inx = (u + nw) * 4 + (lane >> 3);
+      if (u + nw < uo && inx < a.noct) {
+        pn = a.ml_p[inx];
+        stn = a.ml_state[inx];
       }
+      const uint32_t s0 = st >> 29;
+      uint32_t pos = ok ? (st & 0x1fffffffu) + p * nib(s_cum[s0], j) : WS;
+      const uint32_t step = 15u * p;
+      while (__any_sync(kFull, pos < WS)) {
+        const bool v = pos < WS;
+        wappend(o, v && pos < lim, pos);
+        if (v) pos += step;
+      }
+      // next hit of the prime = smallest exit of its 8 class progressions
+      const uint32_t ex = pos - WS;
+      uint32_t m = ex;
+      m = min(m, __shfl_xor_sync(kFull, m, 1));
+      m = min(m, __shfl_xor_sync(kFull, m, 2));
+      m = min(m, __shfl_xor_sync(kFull, m, 4));
+      const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
+      if (ok && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
     }
-    if (ok) a.ml_state[i] = (pos - WS) | (s << 29);
+  }
+  // single ML primes: one per lane (next step's data prefetched)
+  const uint64_t us = (a.nml - a.noct + 31) / 32;
+  {
+    uint64_t u = gw;
+    uint32_t pn = 0, stn = 0;
+    if (u < us && a.noct + u * 32 + lane < a.nml) {
+      pn = a.ml_p[a.noct + u * 32 + lane];
+      stn = a.ml_state[a.noct + u * 32 + lane];
+    }
+    for (; u < us; u += nw) {
+      const uint64_t i = a.noct + u * 32 + lane;
+      const bool ok = i < a.nml;
+      const uint32_t p = pn, st = stn;
+      const uint64_t inx = a.noct + (u + nw) * 32 + lane;
+      if (u + nw < us && inx < a.nml) {
+        pn = a.ml_p[inx];
+        stn = a.ml_state[inx];
+      }
+      uint32_t pos = ok ? (st & 0x1fffffffu) : WS;
+      uint32_t s = st >> 29;
+      while (__any_sync(kFull, pos < WS)) {
+        const bool v = pos < WS;
+        wappend(o, v && pos < lim, pos);
+        if (v) {
+          pos += wheel_D(s) * p;
+          s = (s + 1) & 7;
+        }
+      }
+      if (ok) a.ml_state[i] = (pos - WS) | (s << 29);
+    }
   }
   // far: exactly one hit in this wave, then re-bucket
   const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
@@ -559,7 +583,7 @@ struct BinArgs {
   const uint32_t* recs;
   const uint32_t* rcount;
   uint32_t rcap, nregions;
-  const uint64_t* frecs;
+  const uint64_t* frecs;  // nullable: no far entries
   const uint8_t* fslot;
   const uint32_t* fcount;
   uint32_t fcap;
@@ -574,21 +598,36 @@ struct BinArgs {
 };
 
 constexpr int kBinThreads = 512;
-constexpr int kBinChunk = 8192;  // records per chunk
+constexpr int kBinPer = 16;                          // records per thread per chunk
+constexpr int kBinChunk = kBinThreads * kBinPer;     // 8192 records
+constexpr int kFarPer = 8;
+constexpr int kFarChunk = kBinThreads * kFarPer;     // 4096 far entries
 constexpr int kMaxWaveTiles = 256;
 constexpr int kMaxRing = 256;
+constexpr int kMaxRegionsPerCta = 64;
 
 struct BinSmem {
-  uint32_t a[kBinChunk];  // chunk as loaded
-  uint32_t b[kBinChunk];  // chunk sorted by tile
-  uint32_t cnt[kMaxWaveTiles];
-  uint32_t off[kMaxWaveTiles];
-  uint32_t base[kMaxWaveTiles];
+  union {
+    struct {
+      uint32_t a[kBinChunk];  // chunk as loaded
+      uint32_t b[kBinChunk];  // chunk sorted by tile
+    } r;
+    struct {
+      uint64_t a[kFarChunk];
+      uint64_t b[kFarChunk];
+      uint8_t ka[kFarChunk];
+      uint8_t kb[kFarChunk];
+    } f;
+  } u;
+  uint32_t cnt[kMaxRing];
+  uint32_t off[kMaxRing];
+  uint32_t base[kMaxRing];
+  uint32_t pre[kMaxRegionsPerCta + 1];  // prefix of the CTA's region counts
   uint32_t total;
 };
 
-__device__ __forceinline__ uint32_t block_excl_scan_small(const uint32_t* cnt, uint32_t* off, uint32_t n) {
-  // one warp scans n (<= 256) counters
+__device__ __forceinline__ uint32_t warp_excl_scan(const uint32_t* cnt, uint32_t* off, uint32_t n) {
+  // one warp scans n counters; returns the total
   const uint32_t lane = threadIdx.x & 31;
   uint32_t run = 0;
   for (uint32_t t0 = 0; t0 < n; t0 += 32) {
@@ -605,22 +644,30 @@ __device__ __forceinline__ uint32_t block_excl_scan_small(const uint32_t* cnt, u
   return run;
 }
 
-// Sort one chunk of `n` (<= kBinChunk) u32 keys already in sm.a by bucket
-// key >> shift (< nb buckets) into sm.b and flush each bucket's run to
-// dst[bucket * cap + reserved..] (value = key & vmask).
-__device__ void bin_chunk32(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask, uint32_t* dst,
-                            uint32_t* gcnt, uint32_t cap, int* overflow) {
+// index of the region holding stream position i (pre[] ascending, nr regions)
+__device__ __forceinline__ uint32_t region_of(const uint32_t* pre, uint32_t nr, uint32_t i) {
+  uint32_t lo = 0, hi = nr;  // pre[lo] <= i < pre[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (pre[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Counting sort of sm.u.r.a[0..n) by key >> shift into sm.u.r.b, then one
+// coalesced run per bucket to dst[bucket * cap + reserved ...].
+__device__ void bin_sort_flush(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask, uint32_t* dst,
+                               uint32_t* gcnt, uint32_t cap, int* overflow) {
   const uint32_t tid = threadIdx.x;
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
-  __syncthreads();
-  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.a[i] >> shift], 1u);
+  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.u.r.a[i] >> shift], 1u);
   __syncthreads();
   if (tid < 32) {
-    const uint32_t tot = block_excl_scan_small(sm.cnt, sm.off, nb);
+    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
     if (tid == 0) sm.total = tot;
   }
   uint32_t resv = 0, rc = 0;
-  if (tid >= 32 && tid < 32 + nb) {  // reservations in flight during the placement
+  if (tid >= 32 && tid < 32 + nb) {  // reservation in flight during the placement
     rc = sm.cnt[tid - 32];
     if (rc) resv = atomicAdd(&gcnt[tid - 32], rc);
   }
@@ -628,21 +675,60 @@ __device__ void bin_chunk32(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb
   for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
   for (uint32_t i = tid; i < n; i += blockDim.x) {
-    const uint32_t key = sm.a[i];
+    const uint32_t key = sm.u.r.a[i];
     const uint32_t t = key >> shift;
-    sm.b[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
+    sm.u.r.b[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
   }
   if (tid >= 32 && tid < 32 + nb) {
     sm.base[tid - 32] = resv;
     if (rc && resv + rc > cap) atomicExch(overflow, 1);
   }
   __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
   for (uint32_t i = tid; i < n; i += blockDim.x) {
-    const uint32_t key = sm.b[i];
+    const uint32_t key = sm.u.r.b[i];
     const uint32_t t = key >> shift;
-    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
     EG_CHECK(t < nb && i >= sm.off[t], "bin t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
+    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
     if (slot < cap) dst[(uint64_t)t * cap + slot] = key & vmask;
+  }
+  __syncthreads();
+}
+
+// same for far entries keyed by their ring slot
+__device__ void bin_sort_flush_far(BinSmem& sm, uint32_t n, uint32_t nb, uint64_t* dst, uint32_t* gcnt, uint32_t cap,
+                                   int* overflow) {
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.u.f.ka[i]], 1u);
+  __syncthreads();
+  if (tid < 32) {
+    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
+    if (tid == 0) sm.total = tot;
+  }
+  uint32_t resv = 0, rc = 0;
+  if (tid >= 32 && tid < 32 + nb) {
+    rc = sm.cnt[tid - 32];
+    if (rc) resv = atomicAdd(&gcnt[tid - 32], rc);
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t t = sm.u.f.ka[i];
+    const uint32_t k = sm.off[t] + atomicAdd(&sm.cnt[t], 1u);
+    sm.u.f.b[k] = sm.u.f.a[i];
+    sm.u.f.kb[k] = (uint8_t)t;
+  }
+  if (tid >= 32 && tid < 32 + nb) {
+    sm.base[tid - 32] = resv;
+    if (rc && resv + rc > cap) atomicExch(overflow, 1);
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t t = sm.u.f.kb[i];
+    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
+    if (slot < cap) dst[(uint64_t)t * cap + slot] = sm.u.f.b[i];
   }
   __syncthreads();
 }
@@ -651,42 +737,85 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
   extern __shared__ uint4 smem_raw[];
   BinSmem& sm = *reinterpret_cast<BinSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  const uint32_t smask = (1u << a.log_s) - 1;
-  // hit records: regions round-robin over the CTAs, chunk by chunk
-  for (uint32_t r = blockIdx.x; r < a.nregions; r += gridDim.x) {
-    const uint32_t cnt = a.rcount[r];
-    const uint32_t* src = a.recs + (uint64_t)r * a.rcap;
-    for (uint32_t c0 = 0; c0 < cnt; c0 += kBinChunk) {
-      const uint32_t n = min((uint32_t)kBinChunk, cnt - c0);
-      for (uint32_t i = tid; i < n; i += blockDim.x) sm.a[i] = src[c0 + i];
-      bin_chunk32(sm, n, a.log_s, a.ntiles_w, smask, a.hits, a.hitcnt, a.hcap, a.overflow);
+  // this CTA's contiguous block of k_gen regions
+  const uint32_t per = (a.nregions + gridDim.x - 1) / gridDim.x;
+  const uint32_t rb = min(a.nregions, blockIdx.x * per), re = min(a.nregions, rb + per);
+  const uint32_t nr = re - rb;
+  EG_CHECK(nr <= kMaxRegionsPerCta, "regions per CTA %u", nr);
+  for (uint32_t t = tid; t < kMaxRing; t += blockDim.x) sm.cnt[t] = 0;
+  // ---- hit records: the CTA's regions as one stream, 8192-record chunks ----
+  if (tid < 32) {
+    uint32_t run = 0;
+    for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+      const uint32_t r = r0 + tid;
+      const uint32_t c = r < nr ? a.rcount[rb + r] : 0;
+      uint32_t x = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (tid >= o) x += y;
+      }
+      if (r < nr) sm.pre[r] = run + x - c;
+      run += __shfl_sync(kFull, x, 31);
     }
+    if (tid == 0) sm.pre[nr] = run;
   }
-  // re-bucketed far entries: runs per ring slot (kept simple: per-entry
-  // warp-aggregated append within each region, entries of one region are
-  // mostly a few slots)
+  __syncthreads();
+  const uint32_t ntot = sm.pre[nr];
+  const uint32_t smask = (1u << a.log_s) - 1;
+  uint32_t reg[kBinPer];
+  auto load_chunk = [&](uint32_t c0) {
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k) {
+      const uint32_t i = c0 + tid + k * kBinThreads;
+      if (i < ntot) {
+        const uint32_t r = region_of(sm.pre, nr, i);
+        reg[k] = a.recs[(uint64_t)(rb + r) * a.rcap + (i - sm.pre[r])];
+      }
+    }
+  };
+  if (ntot) load_chunk(0);
+  for (uint32_t c0 = 0; c0 < ntot; c0 += kBinChunk) {
+    const uint32_t n = min((uint32_t)kBinChunk, ntot - c0);
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k)
+      if (tid + k * kBinThreads < n) sm.u.r.a[tid + k * kBinThreads] = reg[k];
+    __syncthreads();
+    if (c0 + kBinChunk < ntot) load_chunk(c0 + kBinChunk);  // next chunk in flight
+    bin_sort_flush(sm, n, a.log_s, a.ntiles_w, smask, a.hits, a.hitcnt, a.hcap, a.overflow);
+  }
+  // ---- re-bucketed far entries, sorted by ring slot ----
   if (a.frecs) {
-    const uint32_t lane = tid & 31;
-    for (uint32_t r = blockIdx.x; r < a.nregions; r += gridDim.x) {
-      const uint32_t cnt = a.fcount[r];
-      const uint64_t* fr = a.frecs + (uint64_t)r * a.fcap;
-      const uint8_t* fs = a.fslot + (uint64_t)r * a.fcap;
-      for (uint32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
-        const uint32_t i = i0 + tid;
-        const bool ok = i < cnt;
-        const uint32_t slot = ok ? fs[i] : 0xffffffffu;
-        const uint32_t part = __ballot_sync(kFull, ok);
-        if (ok) {
-          const uint32_t grp = __match_any_sync(part, slot);
-          const uint32_t leader = __ffs(grp) - 1;
-          uint32_t b = 0;
-          if (lane == leader) b = atomicAdd(&a.far_bcount[slot], (uint32_t)__popc(grp));
-          b = __shfl_sync(grp, b, leader);
-          const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
-          if (pos < a.bcap) a.far_buckets[(uint64_t)slot * a.bcap + pos] = fr[i];
-          else atomicExch(a.overflow, 1);
+    if (tid < 32) {
+      uint32_t run = 0;
+      for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+        const uint32_t r = r0 + tid;
+        const uint32_t c = r < nr ? a.fcount[rb + r] : 0;
+        uint32_t x = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (tid >= o) x += y;
+        }
+        if (r < nr) sm.pre[r] = run + x - c;
+        run += __shfl_sync(kFull, x, 31);
+      }
+      if (tid == 0) sm.pre[nr] = run;
+    }
+    __syncthreads();
+    const uint32_t ftot = sm.pre[nr];
+    for (uint32_t c0 = 0; c0 < ftot; c0 += kFarChunk) {
+      const uint32_t n = min((uint32_t)kFarChunk, ftot - c0);
+#pragma unroll
+      for (int k = 0; k < kFarPer; ++k) {
+        const uint32_t i = c0 + tid + k * kBinThreads;
+        if (i < ftot) {
+          const uint32_t r = region_of(sm.pre, nr, i);
+          const uint64_t src = (uint64_t)(rb + r) * a.fcap + (i - sm.pre[r]);
+          sm.u.f.a[i - c0] = a.frecs[src];
+          sm.u.f.ka[i - c0] = a.fslot[src];
         }
       }
+      __syncthreads();
+      bin_sort_flush_far(sm, n, a.ring, a.far_buckets, a.far_bcount, a.bcap, a.overflow);
     }
   }
 }
