@@ -84,6 +84,12 @@ int erato_gpu_f_from_midpoint(unsigned e, unsigned l, uint64_t n, unsigned flags
 uint64_t erato_gpu_isqrt(uint64_t x);
 /* first_offset, Lemma 1 (src/wheel.cpp:43-47). */
 uint32_t erato_gpu_first_offset(uint32_t p, unsigned l, uint64_t f);
+/* Host twin of the device start-offset logic (sieve_kernels.cuh first_hit):
+ * index offset (c*p - x)/2 of the first multiple c*p >= x (x odd) whose
+ * cofactor c >= cmin is coprime to 30, and c's wheel class (0..7 for
+ * c mod 30 = 1,7,11,13,17,19,23,29).  With x = u this is Lemma 1 +
+ * wheel_align (src/wheel.cpp:43-69) in one step. */
+int erato_gpu_first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint64_t* offset, unsigned* wheel_class);
 /* table_filename (src/driver.cpp:17-20); returns bytes needed incl. NUL. */
 size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, size_t cap);
 /* errc_name (src/params.cpp:7-21) for codes 1..10, plus the GPU codes. */

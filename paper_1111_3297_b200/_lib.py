@@ -21,6 +21,7 @@ EXPORTS = (
     "erato_gpu_table_filename", "erato_gpu_errc_name", "erato_gpu_last_error", "erato_gpu_create",
     "erato_gpu_destroy", "erato_gpu_device_count", "erato_gpu_run", "erato_gpu_sieve_to_host",
     "erato_gpu_count", "erato_gpu_write_table", "erato_gpu_shard", "erato_gpu_extract_primes",
+    "erato_gpu_first_hit",
 )
 
 
@@ -56,6 +57,8 @@ def load(path: str = SO_PATH):
     L.erato_gpu_isqrt.argtypes = [C.c_uint64]
     L.erato_gpu_first_offset.restype = C.c_uint32
     L.erato_gpu_first_offset.argtypes = [C.c_uint32, C.c_uint, C.c_uint64]
+    L.erato_gpu_first_hit.restype = C.c_int
+    L.erato_gpu_first_hit.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, u64p, C.POINTER(C.c_uint)]
     L.erato_gpu_table_filename.restype = C.c_size_t
     L.erato_gpu_table_filename.argtypes = [C.c_uint, C.c_uint64, C.c_uint64, C.c_char_p, C.c_size_t]
     L.erato_gpu_errc_name.restype = C.c_char_p

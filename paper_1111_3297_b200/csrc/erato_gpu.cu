@@ -170,6 +170,30 @@ uint32_t erato_gpu_first_offset(uint32_t p, unsigned l, uint64_t f) {
   return (uint32_t)(r % 2 == 0 ? (p - r - 1) / 2 : (2 * (uint64_t)p - r - 1) / 2);
 }
 
+// host twin of eg::first_hit (same arithmetic, 128-bit quotient)
+int erato_gpu_first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint64_t* offset, unsigned* wheel_class) {
+  static const uint8_t adv[30] = {1, 0, 5, 4, 3, 2, 1, 0, 3, 2, 1, 0, 1, 0, 3, 2, 1, 0, 1, 0, 3, 2, 1, 0, 5, 4, 3, 2, 1, 0};
+  static const uint8_t cls[30] = {255, 0, 255, 255, 255, 255, 255, 1, 255, 255, 255, 2, 255, 3, 255,
+                                  255, 255, 4, 255, 5, 255, 255, 255, 6, 255, 255, 255, 255, 255, 7};
+  if (p < 7 || p % 2 == 0 || p % 3 == 0 || p % 5 == 0 || x % 2 == 0)
+    return fail(ERATO_GPU_E_INVALID_ARG, "first_hit needs p coprime to 30, p >= 7, x odd");
+  uint64_t c = x / p, r = x % p;
+  uint64_t d = 0;
+  if (r) {
+    ++c;
+    d = p - r;
+  }
+  if (c < cmin) {
+    d += (cmin - c) * (uint64_t)p;
+    c = cmin;
+  }
+  const unsigned cm = (unsigned)(c % 30), a = adv[cm];
+  d += (uint64_t)a * p;
+  if (offset) *offset = d >> 1;
+  if (wheel_class) *wheel_class = cls[cm + a];
+  return 0;
+}
+
 // table_filename, /root/reference/proj/src/driver.cpp:17-20
 size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, size_t cap) {
   const std::string s = "erato_l" + std::to_string(l) + "_f" + std::to_string(f) + "_n" +

@@ -764,11 +764,13 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
   const uint32_t smask = (1u << a.log_s) - 1;
   uint32_t reg[kBinPer];
   auto load_chunk = [&](uint32_t c0) {
+    // indices c0 + tid + k*512 grow with k: one search, then a forward walk
+    uint32_t r = c0 + tid < ntot ? region_of(sm.pre, nr, c0 + tid) : 0;
 #pragma unroll
     for (int k = 0; k < kBinPer; ++k) {
       const uint32_t i = c0 + tid + k * kBinThreads;
       if (i < ntot) {
-        const uint32_t r = region_of(sm.pre, nr, i);
+        while (sm.pre[r + 1] <= i) ++r;
         reg[k] = a.recs[(uint64_t)(rb + r) * a.rcap + (i - sm.pre[r])];
       }
     }
@@ -804,11 +806,12 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
     const uint32_t ftot = sm.pre[nr];
     for (uint32_t c0 = 0; c0 < ftot; c0 += kFarChunk) {
       const uint32_t n = min((uint32_t)kFarChunk, ftot - c0);
+      uint32_t r = c0 + tid < ftot ? region_of(sm.pre, nr, c0 + tid) : 0;
 #pragma unroll
       for (int k = 0; k < kFarPer; ++k) {
         const uint32_t i = c0 + tid + k * kBinThreads;
         if (i < ftot) {
-          const uint32_t r = region_of(sm.pre, nr, i);
+          while (sm.pre[r + 1] <= i) ++r;
           const uint64_t src = (uint64_t)(rb + r) * a.fcap + (i - sm.pre[r]);
           sm.u.f.a[i - c0] = a.frecs[src];
           sm.u.f.ka[i - c0] = a.fslot[src];

@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a sieve (through the C ABI) against the reference.
+
+Bar: bit-exact tables and counts.  Small and ragged cases are compared with
+the reference's own run_sieve (oracle/_ref, the unmodified library) and with
+the restated oracle; the five BASELINE configs with the golden pins (count +
+sha256 of the whole table); full-size properties (shard concatenation,
+Miller-Rabin spot checks, extract_primes) cover what the oracle cannot redo
+in seconds.
+"""
+import hashlib
+import os
+import random
+import tempfile
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(t):
+    return hashlib.sha256(np.ascontiguousarray(t).tobytes()).hexdigest()
+
+
+def miller_rabin(n: int) -> bool:
+    # deterministic for 64-bit (tests/support.hpp:28-54 bases)
+    if n < 2:
+        return False
+    bases = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+    for p in bases:
+        if n % p == 0:
+            return n == p
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in bases:
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+SMALL = [(10, 2048, 4, False), (12, 4096, 8, False), (4, 2048, 4, True), (10, 6, 1, False), (10, 5, 1, False),
+         (16, 3, 5, True), (13, 100, 300, True), (17, 9000, 64, False), (20, 523776, 16, False),
+         (18, 1 << 30, 40, False), (12, 1 << 40, 1000, False), (16, 1 << 45, 200, False),
+         (13, (1 << 46) + 12345, 3001, False), (20, 1 << 41, 600, False), (4, 1, 1, True), (5, 2, 7, True),
+         (11, 7, 9, False), (14, 123456789, 17, False)]
+
+
+@pytest.mark.parametrize("l,f,n,tm", SMALL)
+def test_small_vs_reference(gpu_ctx, reference, l, f, n, tm):
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n, test_mode=tm)
+    g, st = gpu_ctx.table(p)
+    r, rc, _ = reference.run_sieve(l, f, n, test_mode=tm)
+    assert st.prime_count == rc
+    assert np.array_equal(g, r)
+
+
+def test_random_pins(gpu_ctx, pins):
+    import paper_1111_3297_b200 as E
+    for rec in pins["random"]:
+        p = E.validate_params(rec["l"], rec["f"], rec["n"], test_mode=True,
+                              allow_overlap=rec.get("allow_overlap", False))
+        g, st = gpu_ctx.table(p)
+        assert st.prime_count == rec["count"], rec
+        assert sha(g) == rec["sha256"], rec
+
+
+def test_random_vs_reference_seeded(gpu_ctx, reference):
+    import paper_1111_3297_b200 as E
+    rng = random.Random(1002)  # acceptance.cpp:71 seed
+    done = 0
+    while done < 40:
+        l = rng.randint(4, 20)
+        n = rng.randint(1, 300)
+        f = rng.randint(1, (1 << rng.randint(l + 2, 50)) >> (l + 1) or 1)
+        try:
+            p = E.validate_params(l, f, n, test_mode=True)
+        except E.Error:
+            continue
+        if p.table_bytes() > 64 << 20:
+            continue
+        g, st = gpu_ctx.table(p)
+        r, rc, _ = reference.run_sieve(l, f, n, test_mode=True)
+        assert st.prime_count == rc and np.array_equal(g, r), (l, f, n)
+        done += 1
+
+
+@pytest.mark.parametrize("l,n", [(17, 64), (12, 50), (10, 1), (4, 3), (20, 64), (16, 40)])
+def test_f0_overlap_convention(gpu_ctx, restated, reference, l, n):
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, 0, n, test_mode=True, allow_overlap=True)
+    g, st = gpu_ctx.table(p)
+    o, oc = restated.bit_table(l, 0, n, test_mode=True, allow_overlap=True)
+    r, rc = reference.f0_table(l, n, test_mode=True)
+    assert st.prime_count == oc == rc
+    assert np.array_equal(g, o) and np.array_equal(g, r)
+
+
+def test_overlap_nonzero_f(gpu_ctx, restated):
+    # u^2 <= v with f > 0 (rejected by the reference; p^2 convention here)
+    import paper_1111_3297_b200 as E
+    for (l, f, n) in [(10, 1, 2049), (12, 3, 5000), (8, 1, 100)]:
+        p = E.validate_params(l, f, n, test_mode=True, allow_overlap=True)
+        g, st = gpu_ctx.table(p)
+        o, oc = restated.bit_table(l, f, n, test_mode=True, allow_overlap=True)
+        assert st.prime_count == oc and np.array_equal(g, o)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_baseline_config_pins(gpu_ctx, pins, cfg):
+    """All five BASELINE configs: count + sha256 of the whole table."""
+    import paper_1111_3297_b200 as E
+    rec = pins["configs"][cfg]
+    p = E.validate_params(rec["l"], rec["f"], rec["n"], allow_overlap=rec["allow_overlap"])
+    g, st = gpu_ctx.table(p)
+    assert g.nbytes == rec["bytes"]
+    assert st.prime_count == rec["count"]
+    assert sha(g) == rec["sha256"]
+    st2 = gpu_ctx.count(p)  # NullSink path agrees
+    assert st2.prime_count == rec["count"]
+
+
+def test_cfg5_shards_concatenate(gpu_ctx, pins):
+    """Range sharding (the multi-GPU decomposition) is exact at full size: 8
+    shard runs of cfg5, hashed in order, give the full-table pin."""
+    import paper_1111_3297_b200 as E
+    rec = pins["configs"]["cfg5"]
+    h = hashlib.sha256()
+    total = 0
+    for r in range(8):
+        fg, ng = E.shard(rec["f"], rec["n"], r, 8)
+        g, st = gpu_ctx.table(E.validate_params(rec["l"], fg, ng))
+        h.update(g.tobytes())
+        total += st.prime_count
+    assert total == rec["count"]
+    assert h.hexdigest() == rec["sha256"]
+
+
+def test_cfg5_miller_rabin_spot_checks(gpu_ctx, pins):
+    import paper_1111_3297_b200 as E
+    rec = pins["configs"]["cfg5"]
+    fg, ng = E.shard(rec["f"], rec["n"], 3, 8)
+    p = E.validate_params(rec["l"], fg, ng)
+    g, _ = gpu_ctx.table(p)
+    rng = np.random.default_rng(17)
+    for j in rng.integers(0, p.table_bits(), 4000):
+        j = int(j)
+        bit = (int(g[j >> 3]) >> (j & 7)) & 1
+        assert bit == (0 if miller_rabin(p.u + 2 * j) else 1), j
+
+
+def test_extract_primes_and_collect_sink(gpu_ctx, reference):
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(16, 1 << 20, 24)
+    primes = gpu_ctx.extract_primes(p)
+    sink = E.PrimeCollectSink()
+    E.run_sieve(p, sink)
+    assert np.array_equal(primes, sink.primes())
+    _, rc, _ = reference.run_sieve(16, 1 << 20, 24)
+    assert len(primes) == rc
+    assert all(miller_rabin(int(x)) for x in primes[:: max(1, len(primes) // 300)])
+    p0 = E.validate_params(12, 0, 8, allow_overlap=True)
+    pr = gpu_ctx.extract_primes(p0)
+    assert int(pr[0]) == 3 and 1 not in set(int(x) for x in pr[:4])
+
+
+def test_run_sieve_sinks_match_reference(gpu_ctx, reference):
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(12, 4096, 8)
+    r, rc, _ = reference.run_sieve(12, 4096, 8)
+    ts = E.TableSink()
+    st = E.run_sieve(p, ts)
+    assert st.prime_count == rc and np.array_equal(ts.bytes(), r)
+    assert E.run_sieve(p, E.NullSink()).prime_count == rc
+
+    class Collect(E.SegmentSink):
+        def __init__(self):
+            self.ts = []
+
+        def on_segment(self, seg, t, params):
+            self.ts.append((t, bytes(seg)))
+
+    c = Collect()
+    E.run_sieve(p, c)
+    assert [t for t, _ in c.ts] == list(range(8))
+    assert b"".join(b for _, b in c.ts) == r.tobytes()
+
+
+def test_file_sink_matches_reference_file(gpu_ctx, reference):
+    import paper_1111_3297_b200 as E
+    with tempfile.TemporaryDirectory() as d1, tempfile.TemporaryDirectory() as d2:
+        p = E.validate_params(10, 2048, 4)
+        path = E.write_table(d1, p)
+        rpath, _ = reference.write_table(d2, 10, 2048, 4)
+        assert os.path.basename(path) == os.path.basename(rpath) == "erato_l10_f2048_n4.bits"
+        assert os.path.getsize(path) == 512  # cli_smoke.sh:25-29
+        assert open(path, "rb").read() == open(rpath, "rb").read()
+        # byte0 bit0 = u = 4194305 = 5 * 838861 -> composite (test_driver.cpp:59-86)
+        assert open(path, "rb").read()[0] & 1 == 1
+
+
+def test_sharded_file_writes(gpu_ctx, reference):
+    """Per-shard pwrite into one file (multi-GPU output) == the whole table."""
+    import paper_1111_3297_b200 as E
+    l, f, n = 16, 1 << 24, 37
+    p = E.validate_params(l, f, n)
+    with tempfile.TemporaryDirectory() as d:
+        for r in (2, 0, 1):
+            fg, ng = E.shard(f, n, r, 3)
+            gpu_ctx.write_table(d, p, fg, ng)
+        data = open(os.path.join(d, E.table_filename(p)), "rb").read()
+    ref, _, _ = reference.run_sieve(l, f, n)
+    assert data == ref.tobytes()
+
+
+def test_edge_cases(gpu_ctx, reference, restated):
+    import paper_1111_3297_b200 as E
+    # v just below 2^64: l = 30, largest f
+    l = 30
+    f = ((1 << 64) >> (l + 1)) - 1
+    p = E.validate_params(l, f, 1)
+    assert p.v < 1 << 64
+    st = gpu_ctx.count(p)
+    assert 0 < st.prime_count < p.table_bits()
+    g, _ = gpu_ctx.table(E.validate_params(10, f << 20, 1))
+    rng = np.random.default_rng(1)
+    pp = E.validate_params(10, f << 20, 1)
+    for j in rng.integers(0, pp.table_bits(), 300):
+        j = int(j)
+        assert ((int(g[j >> 3]) >> (j & 7)) & 1) == (0 if miller_rabin(pp.u + 2 * j) else 1)
+    # errors come back with the reference's codes
+    with pytest.raises(E.Error) as ei:
+        gpu_ctx.count(E.SieveParams(9, 1, 1, 0, 0))
+    assert ei.value.code == E.errc.l_out_of_range
+    with pytest.raises(E.Error) as ei:
+        E.validate_params(10, 0, 1)
+    assert ei.value.code == E.errc.f_zero_or_overlap
+
+
+def test_repeat_runs_deterministic(gpu_ctx):
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(21, (1 << 26) - 2048, 256)
+    a, sa = gpu_ctx.table(p)
+    b, sb = gpu_ctx.table(p)
+    assert sa.prime_count == sb.prime_count and np.array_equal(a, b)

@@ -1,6 +1,6 @@
 """Ad-hoc GPU parity probe (development aid): GPU vs reference on small cases + cfg3."""
 import hashlib, sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1111_3297_b200 as E
 from oracle.oracle import Reference, Restated

@@ -1,6 +1,6 @@
 """Development aid: run one (l, f, n) case on the GPU and compare with the reference."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_1111_3297_b200 as E
 from oracle.oracle import Reference
