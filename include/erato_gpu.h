@@ -104,6 +104,10 @@ const char* erato_gpu_last_error(void);
 typedef struct erato_gpu_ctx erato_gpu_ctx;
 int erato_gpu_create(int device, erato_gpu_ctx** out);
 void erato_gpu_destroy(erato_gpu_ctx* ctx);
+/* Cap on the number of base primes, RunOptions::max_base_pairs / the CLI's
+ * --max-base-pairs (driver.hpp:84, base.cpp:24-27); default 2^27 as in the
+ * reference (base.hpp:87).  Runs above it fail with ALLOC_LIMIT. */
+int erato_gpu_set_max_base_pairs(erato_gpu_ctx* ctx, uint64_t max_pairs);
 /* Number of CUDA devices visible (0 when none). */
 int erato_gpu_device_count(void);
 

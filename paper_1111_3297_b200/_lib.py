@@ -21,7 +21,7 @@ EXPORTS = (
     "erato_gpu_table_filename", "erato_gpu_errc_name", "erato_gpu_last_error", "erato_gpu_create",
     "erato_gpu_destroy", "erato_gpu_device_count", "erato_gpu_run", "erato_gpu_sieve_to_host",
     "erato_gpu_count", "erato_gpu_write_table", "erato_gpu_shard", "erato_gpu_extract_primes",
-    "erato_gpu_first_hit",
+    "erato_gpu_first_hit", "erato_gpu_set_max_base_pairs",
 )
 
 
@@ -69,6 +69,8 @@ def load(path: str = SO_PATH):
     L.erato_gpu_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.erato_gpu_destroy.restype = None
     L.erato_gpu_destroy.argtypes = [C.c_void_p]
+    L.erato_gpu_set_max_base_pairs.restype = C.c_int
+    L.erato_gpu_set_max_base_pairs.argtypes = [C.c_void_p, C.c_uint64]
     L.erato_gpu_device_count.restype = C.c_int
     L.erato_gpu_device_count.argtypes = []
     L.erato_gpu_run.restype = C.c_int

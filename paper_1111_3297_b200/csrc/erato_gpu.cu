@@ -99,6 +99,7 @@ struct erato_gpu_ctx {
   DevBuf base_bits, primes, med, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
   DevBuf recs, rcount, frecs, fslot, fcount;  // k_gen -> k_bin per-warp regions
   double hcap_scale = 1.0, bcap_scale = 1.0;
+  uint64_t max_base_pairs = uint64_t{1} << 27;  // base.hpp:87
   cudaEvent_t ev[4] = {};
   std::vector<cudaEvent_t> phase_ev;  // pairs, grown on demand
 };
@@ -208,6 +209,12 @@ void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_ou
   const unsigned __int128 e = (unsigned __int128)n * (unsigned)(rank + 1) / (unsigned)world;
   *f_out = f + (uint64_t)b;
   *n_out = (uint64_t)(e - b);
+}
+
+int erato_gpu_set_max_base_pairs(erato_gpu_ctx* c, uint64_t max_pairs) {
+  if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
+  c->max_base_pairs = max_pairs;
+  return 0;
 }
 
 int erato_gpu_device_count(void) {
@@ -406,8 +413,9 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     const uint64_t nprimes = hb[0];
     const uint64_t i61 = hb[8], iwarp = std::max(hb[9], hb[8]), iS = hb[10], iWS = hb[11];
     const uint64_t idense = std::max(hb[12], iS);
-    if (nprimes > (uint64_t{1} << 27))
-      return fail(ERATO_GPU_ALLOC_LIMIT, std::to_string(nprimes) + " base primes exceed cap 134217728");
+    if (nprimes > c->max_base_pairs)
+      return fail(ERATO_GPU_ALLOC_LIMIT, std::to_string(nprimes) + " base primes exceed cap " +
+                                              std::to_string(c->max_base_pairs));
     uint32_t pmax = 0;
     if (nprimes) CUDA_TRY(cudaMemcpy(&pmax, c->primes.as<uint32_t>() + nprimes - 1, 4, cudaMemcpyDeviceToHost));
 

@@ -247,6 +247,10 @@ class Context:
         except Exception:
             pass
 
+    def set_max_base_pairs(self, n: int) -> None:
+        """RunOptions::max_base_pairs (driver.hpp:84); default 2^27."""
+        _check(_lib.load().erato_gpu_set_max_base_pairs(self._h, n))
+
     # ---- raw calls ------------------------------------------------------
     def count(self, params: SieveParams) -> RunStats:
         st = _lib.Stats()
@@ -396,6 +400,7 @@ def run_sieve(params: SieveParams, sink: SegmentSink, opt: Optional[RunOptions] 
     """
     opt = opt or RunOptions()
     ctx = context(opt.device)
+    ctx.set_max_base_pairs(opt.max_base_pairs)
     if isinstance(sink, NullSink):
         stats = ctx.count(params)
     elif isinstance(sink, FileSink):
@@ -409,8 +414,6 @@ def run_sieve(params: SieveParams, sink: SegmentSink, opt: Optional[RunOptions] 
             sb = params.segment_bytes()
             for t in range(params.n):
                 sink.on_segment(table[t * sb:(t + 1) * sb], t, params)
-    if stats.base_primes > opt.max_base_pairs:
-        raise Error(errc.alloc_limit, f"{stats.base_primes} base primes exceed cap {opt.max_base_pairs}")
     sink.finish(params)
     stats.segments = params.n
     return stats

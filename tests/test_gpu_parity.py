@@ -226,17 +226,26 @@ def test_edge_cases(gpu_ctx, reference, restated):
     import paper_1111_3297_b200 as E
     # v just below 2^64: l = 30, largest f
     l = 30
-    f = ((1 << 64) >> (l + 1)) - 1
+    f = (((1 << 64) - 1) >> (l + 1)) - 1  # largest valid f for n = 1
     p = E.validate_params(l, f, 1)
-    assert p.v < 1 << 64
+    assert p.v < 1 << 64 and p.v > (1 << 64) - (1 << 32)
+    with pytest.raises(E.Error) as ei:
+        E.validate_params(l, f + 1, 1)
+    assert ei.value.code == E.errc.overflow
+    with pytest.raises(E.Error) as ei:  # 2^32 base primes: over the reference's default cap
+        gpu_ctx.count(p)
+    assert ei.value.code == E.errc.alloc_limit
+    gpu_ctx.set_max_base_pairs(1 << 28)
     st = gpu_ctx.count(p)
     assert 0 < st.prime_count < p.table_bits()
-    g, _ = gpu_ctx.table(E.validate_params(10, f << 20, 1))
+    f10 = (((1 << 64) - 1) >> 11) - 1
+    pp = E.validate_params(10, f10, 1)
+    g, _ = gpu_ctx.table(pp)
     rng = np.random.default_rng(1)
-    pp = E.validate_params(10, f << 20, 1)
     for j in rng.integers(0, pp.table_bits(), 300):
         j = int(j)
         assert ((int(g[j >> 3]) >> (j & 7)) & 1) == (0 if miller_rabin(pp.u + 2 * j) else 1)
+    gpu_ctx.set_max_base_pairs(1 << 27)
     # errors come back with the reference's codes
     with pytest.raises(E.Error) as ei:
         gpu_ctx.count(E.SieveParams(9, 1, 1, 0, 0))
