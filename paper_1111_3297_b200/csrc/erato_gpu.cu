@@ -240,7 +240,7 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8)));
+                                (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
@@ -284,7 +284,7 @@ namespace {
 
 // Launch the tile kernel over `ntiles` tiles starting at `tile0`.
 void launch_tiles(erato_gpu_ctx* c, cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles) {
-  const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8;
+  const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8 + (size_t)a.nmed_warp * 8;
   eg::k_tile<<<ntiles, eg::kTileThreads, smem, st>>>(a);
 }
 
@@ -346,7 +346,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
   P.ntiles = (P.T + P.S - 1) >> P.log_s;
   {
     int occ = 1;
-    const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8;
+    const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8 + eg::kMaxWarpPrimes * 8;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile, eg::kTileThreads, smem));
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
@@ -386,7 +386,8 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
       {
         const auto bw = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), (1u << kBaseLogTile) / 64) - c->h_sp.begin();
-        ta.nmed_warp = (uint32_t)std::min<int64_t>(std::max<int64_t>(bw - b61, 0), ta.nmed);
+        ta.nmed_warp = (uint32_t)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(bw - b61, 0), ta.nmed),
+                                                   eg::kMaxWarpPrimes);
       }
       ta.ptab = c->ptab.as<uint32_t>();
       ta.table = c->base_bits.as<uint32_t>();
@@ -492,7 +493,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.log_s = P.log_s;
     ta.med = c->med.as<uint4>();
     ta.nmed = (uint32_t)nmed;
-    ta.nmed_warp = (uint32_t)std::min<uint64_t>(iwarp - i61, nmed);
+    ta.nmed_warp = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(iwarp - i61, nmed), eg::kMaxWarpPrimes);
     ta.ptab = c->ptab.as<uint32_t>();
     ta.hits = have_large ? c->hits.as<uint32_t>() : nullptr;
     ta.hitcnt = c->hitcnt.as<uint32_t>();

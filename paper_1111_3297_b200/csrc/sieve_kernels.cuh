@@ -185,6 +185,7 @@ struct TileArgs {
 };
 
 constexpr int kTileThreads = 1024;
+constexpr uint32_t kMaxWarpPrimes = 4096;  // medium primes below S/64 (1900 at S = 2^20)
 constexpr int kTileWarps = kTileThreads / 32;
 
 __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
@@ -218,6 +219,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   extern __shared__ uint4 smem4[];
   uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
   uint32_t* const tile = pat + kPatWords;
+  uint2* const s_wq = reinterpret_cast<uint2*>(tile + ((1u << a.log_s) >> 5));  // [nmed_warp] (q0, p | s<<29)
+  __shared__ uint32_t s_item;
   __shared__ unsigned long long s_red[kTileWarps];
   __shared__ uint8_t s_combo[32];
   __shared__ uint32_t s_cum[8];
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
       s_cum[tid] = v;
     }
+    if (tid == 0) s_item = 0;
   }
   __syncthreads();
 
@@ -278,15 +282,24 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     const uint32_t X30 = (uint32_t)(x_t % 30u);
     const uint32_t t = (uint32_t)t64;
     const bool early = a.p2_floor && x_t < ((uint64_t)1 << 42);
-    // 2a. warp-per-prime (p < S/64): lane j takes wheel class (s+j)&7 of
-    // period j>>3; 32 lanes = 4 periods = 60p.  Items in snake order over
-    // the warps (largest work first) for balance.
-    for (uint32_t r = 0;; ++r) {
-      const uint32_t item = r * kTileWarps + ((r & 1) ? (kTileWarps - 1 - warp) : warp);
-      if (item >= a.nmed_warp) break;
+    // 2a. warp-per-prime (p < S/64): start offsets computed lane-parallel into
+    // shared memory, then each warp takes one prime at a time (dynamic, largest
+    // work first); lane j marks wheel class (s+j)&7 of period j>>3 (32 lanes =
+    // 4 periods = 60p).
+    for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
       uint32_t p, s;
-      const uint32_t q0 = med_first(a.med[item], t, X30, x_t, early, s_combo, p, s);
-      uint32_t q = q0 + p * (nib(s_cum[s], lane & 7) + 15u * (lane >> 3));
+      const uint32_t q0 = med_first(a.med[i], t, X30, x_t, early, s_combo, p, s);
+      s_wq[i] = make_uint2(q0, p | (s << 29));
+    }
+    __syncthreads();
+    for (;;) {
+      uint32_t item = 0;
+      if (lane == 0) item = atomicAdd(&s_item, 1u);
+      item = __shfl_sync(kFull, item, 0);
+      if (item >= a.nmed_warp) break;
+      const uint2 w = s_wq[item];
+      const uint32_t p = w.y & 0x1fffffffu, s = w.y >> 29;
+      uint32_t q = w.x + p * (nib(s_cum[s], lane & 7) + 15u * (lane >> 3));
       const uint32_t step = 60u * p;
       for (; q + 3 * step < S; q += 4 * step) {
         mark(tile, q);
@@ -296,7 +309,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       }
       for (; q < S; q += step) mark(tile, q);
     }
-    // 2b. lane-per-prime (S/64 <= p <= S): whole wheel periods unrolled
+    // 2b. lane-per-prime (S/64 <= p <= S): whole wheel periods unrolled for
+    // p <= S/8, a plain wheel walk for the few-mark primes above
     const uint32_t nlane = a.nmed - a.nmed_warp;
     const uint32_t nitem = (nlane + 31) / 32;
     uint32_t item = warp;
@@ -310,27 +324,35 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       if (valid) {
         uint32_t p, s;
         uint32_t q = med_first(cur, t, X30, x_t, early, s_combo, p, s);
-        const uint32_t cp = s_cum[s];
-        const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
-                       o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
-        const uint32_t per = 15u * p;
-        for (; q + o7 < S; q += per) {
-          mark(tile, q);
-          mark(tile, q + o1);
-          mark(tile, q + o2);
-          mark(tile, q + o3);
-          mark(tile, q + o4);
-          mark(tile, q + o5);
-          mark(tile, q + o6);
-          mark(tile, q + o7);
+        if ((p << 3) > S) {
+          while (q < S) {
+            mark(tile, q);
+            q += wheel_D(s) * p;
+            s = (s + 1) & 7;
+          }
+        } else {
+          const uint32_t cp = s_cum[s];
+          const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
+                         o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
+          const uint32_t per = 15u * p;
+          for (; q + o7 < S; q += per) {
+            mark(tile, q);
+            mark(tile, q + o1);
+            mark(tile, q + o2);
+            mark(tile, q + o3);
+            mark(tile, q + o4);
+            mark(tile, q + o5);
+            mark(tile, q + o6);
+            mark(tile, q + o7);
+          }
+          if (q < S) mark(tile, q);
+          if (q + o1 < S) mark(tile, q + o1);
+          if (q + o2 < S) mark(tile, q + o2);
+          if (q + o3 < S) mark(tile, q + o3);
+          if (q + o4 < S) mark(tile, q + o4);
+          if (q + o5 < S) mark(tile, q + o5);
+          if (q + o6 < S) mark(tile, q + o6);
         }
-        if (q < S) mark(tile, q);
-        if (q + o1 < S) mark(tile, q + o1);
-        if (q + o2 < S) mark(tile, q + o2);
-        if (q + o3 < S) mark(tile, q + o3);
-        if (q + o4 < S) mark(tile, q + o4);
-        if (q + o5 < S) mark(tile, q + o5);
-        if (q + o6 < S) mark(tile, q + o6);
       }
     }
   }
