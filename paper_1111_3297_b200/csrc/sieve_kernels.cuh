@@ -458,10 +458,17 @@ struct GenArgs {
   uint8_t* fslot;     // [nwarps][fcap] their ring slot
   uint32_t* fcount;   // [nwarps]
   uint32_t fcap;
+  uint32_t part, nparts;  // this launch walks part `part` of each unit class
   int* overflow;
 };
 
 constexpr int kGenThreads = 512;
+
+// [begin, end) of part `part` out of `nparts` equal slices of [0, n)
+__device__ __forceinline__ void part_range(uint64_t n, uint32_t part, uint32_t nparts, uint64_t& b, uint64_t& e) {
+  b = n * part / nparts;
+  e = n * (part + 1) / nparts;
+}
 
 struct WarpOut {
   uint32_t* rec;
@@ -496,10 +503,11 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
   WarpOut o{a.recs + gw * a.rcap, 0, a.rcap, a.frecs + gw * a.fcap, a.fslot + gw * a.fcap, 0, a.fcap};
 
   // octets: 4 primes per warp-step (next step's data prefetched)
-  const uint64_t uo = (a.noct + 3) / 4;
+  uint64_t ub, uo;
+  part_range((a.noct + 3) / 4, a.part, a.nparts, ub, uo);
   {
     const uint32_t j = lane & 7;
-    uint64_t u = gw;
+    uint64_t u = ub + gw;
     uint32_t pn = 0, stn = 0;
     if (u < uo && u * 4 + (lane >> 3) < a.noct) {
       pn = a.ml_p[u * 4 + (lane >> 3)];
@@ -533,9 +541,10 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     }
   }
   // single ML primes: one per lane (next step's data prefetched)
-  const uint64_t us = (a.nml - a.noct + 31) / 32;
+  uint64_t usb, us;
+  part_range((a.nml - a.noct + 31) / 32, a.part, a.nparts, usb, us);
   {
-    uint64_t u = gw;
+    uint64_t u = usb + gw;
     uint32_t pn = 0, stn = 0;
     if (u < us && a.noct + u * 32 + lane < a.nml) {
       pn = a.ml_p[a.noct + u * 32 + lane];
@@ -565,8 +574,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
   }
   // far: exactly one hit in this wave, then re-bucket
   const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  const uint64_t uf = (nfar + 31) / 32;
-  for (uint64_t u = gw; u < uf; u += nw) {
+  uint64_t ufb, uf;
+  part_range((nfar + 31) / 32, a.part, a.nparts, ufb, uf);
+  for (uint64_t u = ufb + gw; u < uf; u += nw) {
     const uint64_t i = u * 32 + lane;
     const bool ok = i < nfar;
     const uint64_t e = ok ? a.far_in[i] : 0;
