@@ -528,6 +528,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ga.fcount = c->fcount.as<uint32_t>();
       ga.fcap = fcap;
       ga.overflow = reinterpret_cast<int*>(d_scal + 17);
+      ga.inv_ws = 1.0 / (double)P.WS;
       ba.recs = ga.recs;
       ba.rcount = ga.rcount;
       ba.rcap = rcap;
