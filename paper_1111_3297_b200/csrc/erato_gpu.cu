@@ -449,7 +449,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 8));
       {
         const uint64_t gen_warps = (uint64_t)c->nsm * kGenBlocksPerSm * (eg::kGenThreads / 32);
-        const double per_wave = eh * P.W;  // records per wave (upper estimate; parts only shrink it)
+        const double per_wave = eh * P.W;  // records per wave
         rcap = (uint32_t)std::min<double>((per_wave / gen_warps * 1.3 + 2048) * c->hcap_scale, 1u << 30);
         rcap = (rcap + 31) & ~31u;
         fcap = nfar ? (uint32_t)std::min<double>(((double)bcap / gen_warps * 1.3 + 512) * c->bcap_scale, 1u << 30) : 1;
@@ -502,10 +502,6 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.count = d_count;
     ta.p2_floor = P.overlap ? 1 : 0;
     const uint32_t gen_blocks = (uint32_t)c->nsm * kGenBlocksPerSm;
-    // k_gen/k_bin may split a wave into parts (ERATO_GPU_PARTS); measured on
-    // B200 at cfg4/cfg5 one part is fastest (the intermediate is not the limit)
-    uint32_t nparts = 1;
-    if (const char* e = std::getenv("ERATO_GPU_PARTS")) nparts = (uint32_t)std::max(1, std::atoi(e));
     const uint32_t gen_warps = gen_blocks * (eg::kGenThreads / 32);
     const uint32_t bin_blocks = std::max<uint32_t>((uint32_t)c->nsm * 2, (gen_warps + eg::kMaxRegionsPerCta - 1) / eg::kMaxRegionsPerCta);
     eg::GenArgs ga{};
@@ -528,7 +524,6 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ga.fcount = c->fcount.as<uint32_t>();
       ga.fcap = fcap;
       ga.overflow = reinterpret_cast<int*>(d_scal + 17);
-      ga.inv_ws = 1.0 / (double)P.WS;
       ba.recs = ga.recs;
       ba.rcount = ga.rcount;
       ba.rcap = rcap;
@@ -567,19 +562,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        // parts keep the k_gen -> k_bin intermediate L2-sized (buffers reused)
-        for (uint32_t part = 0; part < nparts; ++part) {
-          ga.part = part;
-          ga.nparts = nparts;
-          eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
-          eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
-          launches += 2;
-        }
+        eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
+        eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
         if (timing) {
           CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           ev_pairs.push_back({evi, true});
           evi += 2;
         }
+        launches += 2;
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
       ta.tile0 = tile0;

@@ -458,18 +458,10 @@ struct GenArgs {
   uint8_t* fslot;     // [nwarps][fcap] their ring slot
   uint32_t* fcount;   // [nwarps]
   uint32_t fcap;
-  uint32_t part, nparts;  // this launch walks part `part` of each unit class
-  double inv_ws;
   int* overflow;
 };
 
 constexpr int kGenThreads = 512;
-
-// [begin, end) of part `part` out of `nparts` equal slices of [0, n)
-__device__ __forceinline__ void part_range(uint64_t n, uint32_t part, uint32_t nparts, uint64_t& b, uint64_t& e) {
-  b = n * part / nparts;
-  e = n * (part + 1) / nparts;
-}
 
 struct WarpOut {
   uint32_t* rec;
@@ -504,11 +496,10 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
   WarpOut o{a.recs + gw * a.rcap, 0, a.rcap, a.frecs + gw * a.fcap, a.fslot + gw * a.fcap, 0, a.fcap};
 
   // octets: 4 primes per warp-step (next step's data prefetched)
-  uint64_t ub, uo;
-  part_range((a.noct + 3) / 4, a.part, a.nparts, ub, uo);
+  const uint64_t uo = (a.noct + 3) / 4;
   {
     const uint32_t j = lane & 7;
-    uint64_t u = ub + gw;
+    uint64_t u = gw;
     uint32_t pn = 0, stn = 0;
     if (u < uo && u * 4 + (lane >> 3) < a.noct) {
       pn = a.ml_p[u * 4 + (lane >> 3)];
@@ -542,10 +533,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     }
   }
   // single ML primes: one per lane (next step's data prefetched)
-  uint64_t usb, us;
-  part_range((a.nml - a.noct + 31) / 32, a.part, a.nparts, usb, us);
+  const uint64_t us = (a.nml - a.noct + 31) / 32;
   {
-    uint64_t u = usb + gw;
+    uint64_t u = gw;
     uint32_t pn = 0, stn = 0;
     if (u < us && a.noct + u * 32 + lane < a.nml) {
       pn = a.ml_p[a.noct + u * 32 + lane];
@@ -575,9 +565,8 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
   }
   // far: exactly one hit in this wave, then re-bucket
   const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  uint64_t ufb, uf;
-  part_range((nfar + 31) / 32, a.part, a.nparts, ufb, uf);
-  for (uint64_t u = ufb + gw; u < uf; u += nw) {
+  const uint64_t uf = (nfar + 31) / 32;
+  for (uint64_t u = gw; u < uf; u += nw) {
     const uint64_t i = u * 32 + lane;
     const bool ok = i < nfar;
     const uint64_t e = ok ? a.far_in[i] : 0;
@@ -589,13 +578,11 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     uint64_t ne = 0;
     if (ok) {
       const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
-      uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
-      while (d * WS > q2) --d;
-      while ((d + 1) * WS <= q2) ++d;
+      const uint64_t d = q2 / WS;
       const uint64_t tgt = a.wave + d;
       if (tgt < a.nwaves) {
         keep = true;
-        slot = (uint32_t)tgt % a.ring;
+        slot = (uint32_t)(tgt % a.ring);
         ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
       }
     }
@@ -607,12 +594,8 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     }
     o.fn += __popc(m);
   }
-  // pad the record region to a multiple of 4 (k_bin copies it as uint4);
-  // the sentinel's tile index is >= every wave's tile count
-  const uint32_t n4 = (min(o.n, o.cap) + 3) & ~3u;
-  if (lane < n4 - min(o.n, o.cap)) o.rec[min(o.n, o.cap) + lane] = 0xffffffffu;
   if (lane == 0) {
-    a.rcount[gw] = n4;
+    a.rcount[gw] = min(o.n, o.cap);
     a.fcount[gw] = min(o.fn, o.fcap);
     if (o.n > o.cap || o.fn > o.fcap) atomicExch(a.overflow, 1);
   }
@@ -644,13 +627,12 @@ constexpr int kFarChunk = kBinThreads * kFarPer;     // 4096 far entries
 constexpr int kMaxWaveTiles = 256;
 constexpr int kMaxRing = 256;
 constexpr int kMaxRegionsPerCta = 64;
-constexpr int kMaxPieces = 4 * kMaxRegionsPerCta;
 
 struct BinSmem {
   union {
     struct {
-      uint32_t a[2][kBinChunk];  // chunks as loaded (TMA double buffer)
-      uint32_t b[kBinChunk];     // chunk sorted by tile
+      uint32_t a[kBinChunk];  // chunk as loaded
+      uint32_t b[kBinChunk];  // chunk sorted by tile
     } r;
     struct {
       uint64_t a[kFarChunk];
@@ -663,40 +645,8 @@ struct BinSmem {
   uint32_t off[kMaxRing];
   uint32_t base[kMaxRing];
   uint32_t pre[kMaxRegionsPerCta + 1];  // prefix of the CTA's region counts
-  // record pieces (region, offset, length <= kBinChunk) and chunks of pieces
-  uint32_t pc_r[kMaxPieces], pc_off[kMaxPieces], pc_len[kMaxPieces], pc_dst[kMaxPieces];
-  uint32_t chunk_p[kMaxPieces + 1];  // first piece of each chunk
-  uint32_t nchunks;
   uint32_t total;
-  unsigned long long mbar[2];
 };
-
-// ---- TMA 1-D bulk copy global -> shared with an mbarrier (sm_90+) ----
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(m))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t warp_excl_scan(const uint32_t* cnt, uint32_t* off, uint32_t n) {
   // one warp scans n counters; returns the total
@@ -727,20 +677,12 @@ __device__ __forceinline__ uint32_t region_of(const uint32_t* pre, uint32_t nr, 
   return lo;
 }
 
-// Counting sort of sm.u.r.a[0..n) (n % 4 == 0, sentinel keys have
-// key >> shift >= nb and are dropped) by key >> shift into sm.u.r.b, then
-// each warp flushes whole tile runs to dst[tile * cap + reserved ...].
-__device__ void bin_sort_flush(BinSmem& sm, const uint4* a4, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask,
-                               uint32_t* dst, uint32_t* gcnt, uint32_t cap, int* overflow) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t n4 = n >> 2;
-  for (uint32_t i = tid; i < n4; i += blockDim.x) {
-    const uint4 k = a4[i];
-    if ((k.x >> shift) < nb) atomicAdd(&sm.cnt[k.x >> shift], 1u);
-    if ((k.y >> shift) < nb) atomicAdd(&sm.cnt[k.y >> shift], 1u);
-    if ((k.z >> shift) < nb) atomicAdd(&sm.cnt[k.z >> shift], 1u);
-    if ((k.w >> shift) < nb) atomicAdd(&sm.cnt[k.w >> shift], 1u);
-  }
+// Counting sort of sm.u.r.a[0..n) by key >> shift into sm.u.r.b, then one
+// coalesced run per bucket to dst[bucket * cap + reserved ...].
+__device__ void bin_sort_flush(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask, uint32_t* dst,
+                               uint32_t* gcnt, uint32_t cap, int* overflow) {
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.u.r.a[i] >> shift], 1u);
   __syncthreads();
   if (tid < 32) {
     const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
@@ -752,32 +694,26 @@ __device__ void bin_sort_flush(BinSmem& sm, const uint4* a4, uint32_t n, uint32_
     if (rc) resv = atomicAdd(&gcnt[tid - 32], rc);
   }
   __syncthreads();
-  // placement cursors live in base[] until the reservations land
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.base[t] = sm.off[t];
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
-  for (uint32_t i = tid; i < n4; i += blockDim.x) {
-    const uint4 k = a4[i];
-    uint32_t t;
-    if ((t = k.x >> shift) < nb) sm.u.r.b[atomicAdd(&sm.base[t], 1u)] = k.x;
-    if ((t = k.y >> shift) < nb) sm.u.r.b[atomicAdd(&sm.base[t], 1u)] = k.y;
-    if ((t = k.z >> shift) < nb) sm.u.r.b[atomicAdd(&sm.base[t], 1u)] = k.z;
-    if ((t = k.w >> shift) < nb) sm.u.r.b[atomicAdd(&sm.base[t], 1u)] = k.w;
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t key = sm.u.r.a[i];
+    const uint32_t t = key >> shift;
+    sm.u.r.b[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
   }
-  __syncthreads();
   if (tid >= 32 && tid < 32 + nb) {
     sm.base[tid - 32] = resv;
     if (rc && resv + rc > cap) atomicExch(overflow, 1);
   }
   __syncthreads();
-  // flush: one warp per tile run, consecutive lanes -> consecutive addresses
-  for (uint32_t t = warp; t < nb; t += blockDim.x >> 5) {
-    const uint32_t c = sm.cnt[t], o = sm.off[t], b = sm.base[t];
-    uint32_t* d = dst + (uint64_t)t * cap;
-    for (uint32_t i = lane; i < c; i += 32)
-      if (b + i < cap) d[b + i] = sm.u.r.b[o + i] & vmask;
-  }
-  __syncthreads();
   for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t i = tid; i < n; i += blockDim.x) {
+    const uint32_t key = sm.u.r.b[i];
+    const uint32_t t = key >> shift;
+    EG_CHECK(t < nb && i >= sm.off[t], "bin t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
+    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
+    if (slot < cap) dst[(uint64_t)t * cap + slot] = key & vmask;
+  }
   __syncthreads();
 }
 
@@ -829,60 +765,47 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
   const uint32_t nr = re - rb;
   EG_CHECK(nr <= kMaxRegionsPerCta, "regions per CTA %u", nr);
   for (uint32_t t = tid; t < kMaxRing; t += blockDim.x) sm.cnt[t] = 0;
-  // ---- hit records: chunks of whole regions (regions are padded to 4
-  // records and capped by kBinChunk), streamed in by TMA bulk copies into a
-  // double buffer so chunk c+1 lands while chunk c is sorted ----
-  const uint32_t smask = (1u << a.log_s) - 1;
-  if (tid == 0) {
-    // pieces of <= kBinChunk records, greedily grouped into chunks
-    uint32_t np = 0, nc = 0, fill = kBinChunk + 1;
-    for (uint32_t r = 0; r < nr; ++r) {
-      const uint32_t cnt = a.rcount[rb + r];
-      for (uint32_t o = 0; o < cnt && np < (uint32_t)kMaxPieces; o += kBinChunk) {
-        const uint32_t len = min((uint32_t)kBinChunk, cnt - o);
-        if (fill + len > (uint32_t)kBinChunk) {
-          sm.chunk_p[nc++] = np;
-          fill = 0;
-        }
-        sm.pc_r[np] = r;
-        sm.pc_off[np] = o;
-        sm.pc_len[np] = len;
-        sm.pc_dst[np] = fill;
-        fill += len;
-        ++np;
+  // ---- hit records: the CTA's regions as one stream, 8192-record chunks ----
+  if (tid < 32) {
+    uint32_t run = 0;
+    for (uint32_t r0 = 0; r0 < nr; r0 += 32) {
+      const uint32_t r = r0 + tid;
+      const uint32_t c = r < nr ? a.rcount[rb + r] : 0;
+      uint32_t x = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (tid >= o) x += y;
       }
+      if (r < nr) sm.pre[r] = run + x - c;
+      run += __shfl_sync(kFull, x, 31);
     }
-    EG_CHECK(np < (uint32_t)kMaxPieces, "pieces %u", np);
-    sm.chunk_p[nc] = np;
-    sm.nchunks = nc;
-    mbar_init(&sm.mbar[0], 1);
-    mbar_init(&sm.mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (tid == 0) sm.pre[nr] = run;
   }
   __syncthreads();
-  const uint32_t nch = sm.nchunks;
-  auto chunk_len = [&](uint32_t c) {
-    const uint32_t last = sm.chunk_p[c + 1] - 1;
-    return sm.pc_dst[last] + sm.pc_len[last];
-  };
-  auto issue = [&](uint32_t c) {  // thread 0 only
-    unsigned long long* m = &sm.mbar[c & 1];
-    mbar_expect_tx(m, chunk_len(c) * 4);
-    uint32_t* dst = sm.u.r.a[c & 1];
-    for (uint32_t k = sm.chunk_p[c]; k < sm.chunk_p[c + 1]; ++k)
-      if (sm.pc_len[k])
-        bulk_g2s(dst + sm.pc_dst[k], a.recs + (uint64_t)(rb + sm.pc_r[k]) * a.rcap + sm.pc_off[k], sm.pc_len[k] * 4, m);
-  };
-  if (tid == 0 && nch > 0) issue(0);
-  for (uint32_t c = 0; c < nch; ++c) {
-    if (tid == 0 && c + 1 < nch) {
-      fence_proxy_async();  // buffer (c+1)&1 was read by chunk c-1's sort
-      issue(c + 1);
+  const uint32_t ntot = sm.pre[nr];
+  const uint32_t smask = (1u << a.log_s) - 1;
+  uint32_t reg[kBinPer];
+  auto load_chunk = [&](uint32_t c0) {
+    // indices c0 + tid + k*512 grow with k: one search, then a forward walk
+    uint32_t r = c0 + tid < ntot ? region_of(sm.pre, nr, c0 + tid) : 0;
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k) {
+      const uint32_t i = c0 + tid + k * kBinThreads;
+      if (i < ntot) {
+        while (sm.pre[r + 1] <= i) ++r;
+        reg[k] = a.recs[(uint64_t)(rb + r) * a.rcap + (i - sm.pre[r])];
+      }
     }
-    mbar_wait(&sm.mbar[c & 1], (c >> 1) & 1);
-    const uint32_t n = chunk_len(c);
-    bin_sort_flush(sm, reinterpret_cast<const uint4*>(sm.u.r.a[c & 1]), n, a.log_s, a.ntiles_w, smask, a.hits,
-                   a.hitcnt, a.hcap, a.overflow);
+  };
+  if (ntot) load_chunk(0);
+  for (uint32_t c0 = 0; c0 < ntot; c0 += kBinChunk) {
+    const uint32_t n = min((uint32_t)kBinChunk, ntot - c0);
+#pragma unroll
+    for (int k = 0; k < kBinPer; ++k)
+      if (tid + k * kBinThreads < n) sm.u.r.a[tid + k * kBinThreads] = reg[k];
+    __syncthreads();
+    if (c0 + kBinChunk < ntot) load_chunk(c0 + kBinChunk);  // next chunk in flight
+    bin_sort_flush(sm, n, a.log_s, a.ntiles_w, smask, a.hits, a.hitcnt, a.hcap, a.overflow);
   }
   // ---- re-bucketed far entries, sorted by ring slot ----
   if (a.frecs) {
