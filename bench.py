@@ -54,6 +54,12 @@ ROOF = {
     4: (19_421_366_720, 7_608_331_782),
     5: (174_787_646_624, 37_185_502_020),
 }
+# Hit records of large primes in this implementation (mod-30 wheel, 2^20-bit
+# tiles), tools/roofline_counts.py `ours_large_records`: k_bin moves 8 B per record.
+LARGE_RECORDS = {1: 0, 2: 0, 3: 20_188, 4: 835_065_655, 5: 7_429_219_143}
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
+# (profiles/r01_ncu_summary.txt, cfg5 wave 100)
+NCU_TRAFFIC = {5: {"k_bin": 206.2e6 + 153.1e6, "k_gen": 132.9e6 + 186.5e6, "k_tile": 133.8e6 + 3.9e6}}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 R_ATOM_MEASURED = 3.47e12  # smem atomicOr/s per B200, microbench/mb_atomics.cu (profiles/r01_microbench_atomics.log)
 
@@ -210,6 +216,31 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
     e2e_value = numbers * args.steps / t_e2e
+    # e2e with the whole table copied to pinned host memory every step
+    e2e_table = None
+    if not args.no_table_e2e:
+        import ctypes as C
+        host = torch.empty(params.table_bytes(), dtype=torch.uint8, pin_memory=True)
+        tt_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st_t = _lib.Stats()
+            rc = _lib.load().erato_gpu_sieve_to_host(ctx.handle, params.l, params.f, params.n, params.flags,
+                                                     C.cast(C.c_void_p(host.data_ptr()), _lib.u8p),
+                                                     host.numel(), C.byref(st_t))
+            if rc:
+                E.erato._check(rc)
+            tt_times.append(time.perf_counter() - t0)
+        t_tab = sum(tt_times) / len(tt_times)
+        if world > 1:
+            tt = torch.tensor([t_tab], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_tab = float(tt.item())
+        e2e_table = {"value": numbers / t_tab, "unit": "numbers/s", "h2d_bytes_per_step": 32 * world,
+                     "d2h_bytes_per_step": params.table_bytes() * world + 116 * world,
+                     "api": "erato_gpu_sieve_to_host (TableSink semantics: whole bit table to pinned host memory)"}
 
     if rank != 0:
         if world > 1:
@@ -222,14 +253,35 @@ def run_ours(args):
     t_atom = A / R_ATOM_MEASURED
     bound = "hbm" if t_hbm >= t_atom else "atomic"
     achieved_gbs = B / (ms / 1e3) / 1e9 / world  # per GPU, each GPU does 1/world of B
+    # dominant kernel (largest device time in the phase-timed pass)
+    split = {"k_tile": ph.small_s, "k_gen": ph.gen_s, "k_bin": ph.bin_s}
+    dom = max(split, key=split.get)
+    waves = max(ph.waves, 1)
+    recs = LARGE_RECORDS[args.config] / world
+    alg = {  # algorithmic bytes per launch
+        "k_bin": 8.0 * recs / waves,                                   # read + write each record
+        "k_gen": (4.0 * recs + 8.0 * ph.base_primes) / waves,          # records out + prime state
+        "k_tile": (params.table_bytes() + 4.0 * recs) / waves,         # table out + records in
+    }
+    launch_s = split[dom] / waves
+    dom_gbs = alg[dom] / launch_s / 1e9 if launch_s > 0 else 0.0
     roof = {
         "bound": "hbm",
-        "achieved": round(achieved_gbs, 1),
+        "kernel": dom,
+        "achieved": round(dom_gbs, 1),
         "peak": hbm,
         "unit": "GB/s",
-        "frac": round(achieved_gbs / hbm, 4),
-        "traffic": None,
+        "frac": round(dom_gbs / hbm, 4),
+        "traffic": NCU_TRAFFIC.get(args.config, {}).get(dom),
+        "alg_bytes_per_launch": alg[dom],
+        "launch_us": round(launch_s * 1e6, 2),
         "peak_source": hbm_src,
+    }
+    run_roof = {
+        "bound": bound,
+        "definition": "north star: t_roof = max(B/BW_HBM, A/R_atom) for the whole run (SURVEY.md 8d)",
+        "achieved_gbs": round(achieved_gbs, 1),
+        "frac_hbm": round(achieved_gbs / hbm, 4),
         "algorithmic_bytes_per_step": B,
         "shared_atomics_per_step": A,
         "atomic_rate_achieved": round(A / (ms / 1e3) / world, 1),
@@ -237,8 +289,8 @@ def run_ours(args):
         "t_roof_ms": round(max(t_hbm, t_atom) * 1e3 / world, 3),
         "binding_term": bound,
         "frac_of_roofline": round(max(t_hbm, t_atom) / world / (ms / 1e3), 4),
-        "kernel_split_ms": {"tile": round(ph.small_s * 1e3, 3), "scatter": round(ph.large_s * 1e3, 3),
-                            "init": round(ph.init_s * 1e3, 3)},
+        "kernel_split_ms": {"k_tile": round(ph.small_s * 1e3, 3), "k_gen": round(ph.gen_s * 1e3, 3),
+                            "k_bin": round(ph.bin_s * 1e3, 3), "init": round(ph.init_s * 1e3, 3)},
     }
     line = {
         "metric": METRIC,
@@ -259,9 +311,11 @@ def run_ours(args):
                    "parallelism": f"range-shard x{world}"},
         "e2e": {"value": e2e_value, "unit": "numbers/s", "h2d_bytes_per_step": 32 * world,
                 "d2h_bytes_per_step": 116 * world,
-                "api": "erato_gpu_count (C ABI, NullSink semantics; includes base primes + init)"},
+                "api": "erato_gpu_count (C ABI, NullSink semantics as the reference bench; includes base primes + init)"},
+        "e2e_table": e2e_table,
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roof,
+        "roofline_run": run_roof,
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -387,6 +441,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=8.0, help="seconds of reference segment work per process")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-table-e2e", action="store_true", help="skip the table-to-host e2e measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -71,6 +71,9 @@ typedef struct {
   uint32_t waves;
   uint32_t kernel_launches;
   uint32_t retries; /* capacity re-runs after a bucket overflow */
+  double gen_s;     /* with ERATO_GPU_PHASE_TIMING: k_gen (large-prime walk) */
+  double bin_s;     /* with ERATO_GPU_PHASE_TIMING: k_bin (hit-record sort) */
+  uint64_t large_records; /* hit records of large primes (written by k_gen) */
 } erato_gpu_stats;
 
 /* ---- host-side parameter logic (no device needed) ---------------------- */

@@ -33,6 +33,7 @@ class Stats(C.Structure):
         ("base_primes", C.c_uint64), ("tiles", C.c_uint64),
         ("log_tile", C.c_uint32), ("waves", C.c_uint32),
         ("kernel_launches", C.c_uint32), ("retries", C.c_uint32),
+        ("gen_s", C.c_double), ("bin_s", C.c_double), ("large_records", C.c_uint64),
     ]
 
 

@@ -543,7 +543,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ba.overflow = ga.overflow;
     }
     const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
-    const size_t nev = timing ? (size_t)P.nwaves * 6 : 0;
+    const size_t nev = timing ? (size_t)P.nwaves * 5 + 8 : 0;
     while (c->phase_ev.size() < nev) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
@@ -563,11 +563,12 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
         eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
+        if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
         eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
         if (timing) {
-          CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
+          CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 2], st));
           ev_pairs.push_back({evi, true});
-          evi += 2;
+          evi += 3;
         }
         launches += 2;
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
@@ -619,12 +620,21 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       stats->init_s = t_init * 1e-3;
       stats->small_s = (t_tot - t_init) * 1e-3;
       if (timing) {
-        double ts = 0, tl = 0;
+        double ts = 0, tl = 0, tg = 0, tb = 0;
         for (const auto& pr : ev_pairs) {
-          float ms = 0;
+          float ms = 0, ms2 = 0;
           cudaEventElapsedTime(&ms, c->phase_ev[pr.first], c->phase_ev[pr.first + 1]);
-          (pr.second ? tl : ts) += ms;
+          if (pr.second) {
+            cudaEventElapsedTime(&ms2, c->phase_ev[pr.first + 1], c->phase_ev[pr.first + 2]);
+            tg += ms;
+            tb += ms2;
+            tl += ms + ms2;
+          } else {
+            ts += ms;
+          }
         }
+        stats->gen_s = tg * 1e-3;
+        stats->bin_s = tb * 1e-3;
         stats->small_s = ts * 1e-3;
         stats->large_s = tl * 1e-3;
       }

@@ -205,13 +205,16 @@ class RunStats:
     waves: int = 0
     kernel_launches: int = 0
     retries: int = 0
+    gen_s: float = 0.0
+    bin_s: float = 0.0
+    large_records: int = 0
 
     @classmethod
     def _from(cls, s: _lib.Stats) -> "RunStats":
         return cls(prime_count=s.prime_count, segments=s.segments, init_s=s.init_s, medium_s=s.small_s,
                    large_s=s.large_s, output_s=s.output_s, total_s=s.total_s, base_primes=s.base_primes,
                    tiles=s.tiles, log_tile=s.log_tile, waves=s.waves, kernel_launches=s.kernel_launches,
-                   retries=s.retries)
+                   retries=s.retries, gen_s=s.gen_s, bin_s=s.bin_s, large_records=s.large_records)
 
 
 @dataclass
