@@ -594,8 +594,12 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     }
     o.fn += __popc(m);
   }
+  // pad the record region to a multiple of 4 records (k_bin loads uint4);
+  // the sentinel's tile index is above every wave's tile count
+  const uint32_t nv = min(o.n, o.cap), n4 = min((nv + 3) & ~3u, o.cap);
+  if (lane < n4 - nv) o.rec[nv + lane] = 0xffffffffu;
   if (lane == 0) {
-    a.rcount[gw] = min(o.n, o.cap);
+    a.rcount[gw] = n4;
     a.fcount[gw] = min(o.fn, o.fcap);
     if (o.n > o.cap || o.fn > o.fcap) atomicExch(a.overflow, 1);
   }
@@ -641,9 +645,9 @@ struct BinSmem {
       uint8_t kb[kFarChunk];
     } f;
   } u;
-  uint32_t cnt[kMaxRing];
-  uint32_t off[kMaxRing];
-  uint32_t base[kMaxRing];
+  uint32_t cnt[kMaxRing + 1];  // [nb]: spill bucket of the sentinels
+  uint32_t off[kMaxRing + 1];
+  uint32_t base[kMaxRing + 1];
   uint32_t pre[kMaxRegionsPerCta + 1];  // prefix of the CTA's region counts
   uint32_t total;
 };
@@ -677,16 +681,27 @@ __device__ __forceinline__ uint32_t region_of(const uint32_t* pre, uint32_t nr, 
   return lo;
 }
 
-// Counting sort of sm.u.r.a[0..n) by key >> shift into sm.u.r.b, then one
-// coalesced run per bucket to dst[bucket * cap + reserved ...].
+// Counting sort of sm.u.r.a[0..n) (n % 4 == 0; sentinels have key >> shift
+// >= nb and land in the spill bucket nb, after the real records) by
+// key >> shift into sm.u.r.b, then one coalesced run per bucket to
+// dst[bucket * cap + reserved ...].
 __device__ void bin_sort_flush(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t nb, uint32_t vmask, uint32_t* dst,
                                uint32_t* gcnt, uint32_t cap, int* overflow) {
   const uint32_t tid = threadIdx.x;
-  for (uint32_t i = tid; i < n; i += blockDim.x) atomicAdd(&sm.cnt[sm.u.r.a[i] >> shift], 1u);
+  const uint4* a4 = reinterpret_cast<const uint4*>(sm.u.r.a);
+  const uint32_t n4 = n >> 2;
+  for (uint32_t i = tid; i < n4; i += blockDim.x) {
+    const uint4 k = a4[i];
+    atomicAdd(&sm.cnt[min(k.x >> shift, nb)], 1u);
+    atomicAdd(&sm.cnt[min(k.y >> shift, nb)], 1u);
+    atomicAdd(&sm.cnt[min(k.z >> shift, nb)], 1u);
+    atomicAdd(&sm.cnt[min(k.w >> shift, nb)], 1u);
+  }
   __syncthreads();
   if (tid < 32) {
-    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
-    if (tid == 0) sm.total = tot;
+    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb + 1);  // off[nb] = real total
+    if (tid == 0) sm.total = sm.off[nb];
+    (void)tot;
   }
   uint32_t resv = 0, rc = 0;
   if (tid >= 32 && tid < 32 + nb) {  // reservation in flight during the placement
@@ -694,20 +709,29 @@ __device__ void bin_sort_flush(BinSmem& sm, uint32_t n, uint32_t shift, uint32_t
     if (rc) resv = atomicAdd(&gcnt[tid - 32], rc);
   }
   __syncthreads();
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t t = tid; t <= nb; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
-  for (uint32_t i = tid; i < n; i += blockDim.x) {
-    const uint32_t key = sm.u.r.a[i];
-    const uint32_t t = key >> shift;
-    sm.u.r.b[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
+  for (uint32_t i = tid; i < n4; i += blockDim.x) {
+    const uint4 k = a4[i];
+    const uint32_t t0 = min(k.x >> shift, nb), t1 = min(k.y >> shift, nb), t2 = min(k.z >> shift, nb),
+                   t3 = min(k.w >> shift, nb);
+    const uint32_t s0 = sm.off[t0] + atomicAdd(&sm.cnt[t0], 1u);
+    const uint32_t s1 = sm.off[t1] + atomicAdd(&sm.cnt[t1], 1u);
+    const uint32_t s2 = sm.off[t2] + atomicAdd(&sm.cnt[t2], 1u);
+    const uint32_t s3 = sm.off[t3] + atomicAdd(&sm.cnt[t3], 1u);
+    sm.u.r.b[s0] = k.x;
+    sm.u.r.b[s1] = k.y;
+    sm.u.r.b[s2] = k.z;
+    sm.u.r.b[s3] = k.w;
   }
   if (tid >= 32 && tid < 32 + nb) {
     sm.base[tid - 32] = resv;
     if (rc && resv + rc > cap) atomicExch(overflow, 1);
   }
   __syncthreads();
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
-  for (uint32_t i = tid; i < n; i += blockDim.x) {
+  for (uint32_t t = tid; t <= nb; t += blockDim.x) sm.cnt[t] = 0;
+  const uint32_t total = sm.total;
+  for (uint32_t i = tid; i < total; i += blockDim.x) {
     const uint32_t key = sm.u.r.b[i];
     const uint32_t t = key >> shift;
     EG_CHECK(t < nb && i >= sm.off[t], "bin t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
@@ -782,27 +806,30 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
     if (tid == 0) sm.pre[nr] = run;
   }
   __syncthreads();
-  const uint32_t ntot = sm.pre[nr];
+  const uint32_t ntot = sm.pre[nr];  // multiple of 4: every region is padded
   const uint32_t smask = (1u << a.log_s) - 1;
-  uint32_t reg[kBinPer];
+  constexpr int kPer4 = kBinPer / 4;
+  uint4 reg[kPer4];
   auto load_chunk = [&](uint32_t c0) {
-    // indices c0 + tid + k*512 grow with k: one search, then a forward walk
-    uint32_t r = c0 + tid < ntot ? region_of(sm.pre, nr, c0 + tid) : 0;
+    // uint4 units c0/4 + tid + k*512 grow with k: one search, then forward walks
+    const uint32_t i0 = c0 + 4 * tid;
+    uint32_t r = i0 < ntot ? region_of(sm.pre, nr, i0) : 0;
 #pragma unroll
-    for (int k = 0; k < kBinPer; ++k) {
-      const uint32_t i = c0 + tid + k * kBinThreads;
+    for (int k = 0; k < kPer4; ++k) {
+      const uint32_t i = i0 + 4 * k * kBinThreads;
       if (i < ntot) {
         while (sm.pre[r + 1] <= i) ++r;
-        reg[k] = a.recs[(uint64_t)(rb + r) * a.rcap + (i - sm.pre[r])];
+        reg[k] = *reinterpret_cast<const uint4*>(a.recs + (uint64_t)(rb + r) * a.rcap + (i - sm.pre[r]));
       }
     }
   };
   if (ntot) load_chunk(0);
   for (uint32_t c0 = 0; c0 < ntot; c0 += kBinChunk) {
     const uint32_t n = min((uint32_t)kBinChunk, ntot - c0);
+    uint4* a4 = reinterpret_cast<uint4*>(sm.u.r.a);
 #pragma unroll
-    for (int k = 0; k < kBinPer; ++k)
-      if (tid + k * kBinThreads < n) sm.u.r.a[tid + k * kBinThreads] = reg[k];
+    for (int k = 0; k < kPer4; ++k)
+      if (4 * (tid + k * kBinThreads) < n) a4[tid + k * kBinThreads] = reg[k];
     __syncthreads();
     if (c0 + kBinChunk < ntot) load_chunk(c0 + kBinChunk);  // next chunk in flight
     bin_sort_flush(sm, n, a.log_s, a.ntiles_w, smask, a.hits, a.hitcnt, a.hcap, a.overflow);
