@@ -243,6 +243,8 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
                                 (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(eg::FusedSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure(8192 * 16));
@@ -542,6 +544,30 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
+    // large-prime path: k_gen + k_bin (default), or the experimental fused
+    // walk+sort kernel (ERATO_GPU_SCATTER=fused; measured 1.5x slower on B200)
+    const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
+    const bool fused = sc_env && std::strcmp(sc_env, "fused") == 0 && ring <= (uint32_t)eg::kFsBins &&
+                       P.W <= (uint32_t)eg::kFsBins;
+    eg::FusedArgs fa{};
+    if (have_large) {
+      fa.ml_p = ga.ml_p;
+      fa.ml_state = ga.ml_state;
+      fa.nml = ga.nml;
+      fa.noct = ga.noct;
+      fa.far_buckets = c->buckets.as<uint64_t>();
+      fa.far_bcount = c->bcount.as<uint32_t>();
+      fa.bcap = bcap;
+      fa.ring = ring;
+      fa.nwaves = P.nwaves;
+      fa.WS = P.WS;
+      fa.log_s = P.log_s;
+      fa.inv_ws = 1.0 / (double)P.WS;
+      fa.hits = c->hits.as<uint32_t>();
+      fa.hitcnt = c->hitcnt.as<uint32_t>();
+      fa.hcap = hcap;
+      fa.overflow = ga.overflow;
+    }
     const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
     const size_t nev = timing ? (size_t)P.nwaves * 5 + 8 : 0;
     while (c->phase_ev.size() < nev) {
@@ -562,15 +588,25 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
-        if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
-        eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
+        if (fused) {
+          fa.wave = w;
+          fa.ntiles_w = ntw;
+          fa.far_in = ga.far_in;
+          fa.far_in_count = ga.far_in_count;
+          eg::k_scatter_fused<<<c->nsm, eg::kFsThreads, sizeof(eg::FusedSmem), st>>>(fa);
+          if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
+          launches += 1;
+        } else {
+          eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
+          if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
+          eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);
+          launches += 2;
+        }
         if (timing) {
           CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 2], st));
           ev_pairs.push_back({evi, true});
           evi += 3;
         }
-        launches += 2;
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
       ta.tile0 = tile0;

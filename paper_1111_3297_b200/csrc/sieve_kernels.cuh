@@ -873,6 +873,301 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_scatter_fused: the large-prime path of one wave in ONE kernel.
+// Each warp walks its share of the large primes — octets of 8 lanes per ML
+// prime with p <= WS/8 (lane j: wheel class (s+j)&7, step 15p), one lane per
+// ML prime above, one lane per entry of the wave's far bucket — and appends
+// one record (its position in the wave) per wheel-admissible multiple to its
+// private shared-memory region (ballot/popc compaction, no atomics).  When
+// the next step could overflow a region the warp pauses (its walk state
+// stays in registers) and the CTA runs a round: counting sort of all staged
+// records by tile, one global atomicAdd per (round, tile) reserving a run,
+// coalesced flushes into the per-tile hit lists.  Far entries re-bucketed
+// into the wave of their next hit (Lemma 2) are staged and
+// flushed the same way by ring slot.  Records never reach HBM unsorted.
+struct FusedArgs {
+  const uint32_t* ml_p;  // ML primes, ascending
+  uint32_t* ml_state;    // pos | s << 29
+  uint32_t nml, noct;    // the first noct ML primes are walked by octets
+  const uint64_t* far_in;  // far bucket of this wave
+  const uint32_t* far_in_count;
+  uint64_t* far_buckets;  // [ring][bcap]
+  uint32_t* far_bcount;
+  uint32_t bcap, ring;
+  uint64_t wave, nwaves;
+  uint32_t WS, ntiles_w, log_s;
+  double inv_ws;
+  uint32_t* hits;    // [ntiles_w][hcap]
+  uint32_t* hitcnt;  // [ntiles_w]
+  uint32_t hcap;
+  int* overflow;
+};
+
+constexpr int kFsThreads = 1024;
+constexpr int kFsWarps = kFsThreads / 32;
+constexpr int kFsRegion = 640;  // staged records per warp
+constexpr int kFsFar = 64;      // staged re-bucketed far entries per warp
+constexpr int kFsBins = 256;    // >= tiles per wave and >= ring slots
+
+struct FusedSmem {
+  uint32_t reg[kFsWarps * kFsRegion];  // staged records, warp w at [w * kFsRegion]
+  uint32_t srt[kFsWarps * kFsRegion];  // sorted by tile
+  uint64_t freg[kFsWarps * kFsFar];
+  uint64_t fsrt[kFsWarps * kFsFar];
+  uint8_t fslot[kFsWarps * kFsFar];
+  uint8_t fsrt_slot[kFsWarps * kFsFar];
+  uint32_t fill[kFsWarps], ffill[kFsWarps];
+  uint32_t cnt[kFsBins], off[kFsBins], base[kFsBins];
+  uint32_t fcnt[kFsBins], foff[kFsBins], fbase[kFsBins];
+  uint32_t cum[8];
+  uint32_t total, ftotal;
+};
+
+// sort the staged records of all warps by tile (far entries by slot), flush
+__device__ void fs_flush(FusedSmem& sm, const FusedArgs& a) {
+  const uint32_t tid = threadIdx.x, nb = a.ntiles_w, shift = a.log_s, ring = a.ring;
+  constexpr uint32_t R = kFsRegion, F = kFsFar;
+  // count
+  for (uint32_t i = tid; i < kFsWarps * R; i += blockDim.x)
+    if (i % R < sm.fill[i / R]) atomicAdd(&sm.cnt[sm.reg[i] >> shift], 1u);
+  for (uint32_t i = tid; i < kFsWarps * F; i += blockDim.x)
+    if (i % F < sm.ffill[i / F]) atomicAdd(&sm.fcnt[sm.fslot[i]], 1u);
+  __syncthreads();
+  if (tid < 32) {
+    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
+    if (tid == 0) sm.total = tot;
+  } else if (tid < 64) {
+    const uint32_t tot = warp_excl_scan(sm.fcnt, sm.foff, ring);
+    if (tid == 32) sm.ftotal = tot;
+  }
+  // global reservations, in flight during the placement
+  uint32_t resv = 0, rc = 0;
+  const bool rt = tid >= 64 && tid < 64 + nb;
+  const bool rf = tid >= 64 + kFsBins && tid < 64 + kFsBins + ring;
+  if (rt) {
+    rc = sm.cnt[tid - 64];
+    if (rc) resv = atomicAdd(&a.hitcnt[tid - 64], rc);
+  } else if (rf) {
+    rc = sm.fcnt[tid - 64 - kFsBins];
+    if (rc) resv = atomicAdd(&a.far_bcount[tid - 64 - kFsBins], rc);
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t t = tid; t < ring; t += blockDim.x) sm.fcnt[t] = 0;
+  __syncthreads();
+  // place
+  for (uint32_t i = tid; i < kFsWarps * R; i += blockDim.x)
+    if (i % R < sm.fill[i / R]) {
+      const uint32_t key = sm.reg[i];
+      const uint32_t t = key >> shift;
+      sm.srt[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
+    }
+  for (uint32_t i = tid; i < kFsWarps * F; i += blockDim.x)
+    if (i % F < sm.ffill[i / F]) {
+      const uint32_t t = sm.fslot[i];
+      const uint32_t k = sm.foff[t] + atomicAdd(&sm.fcnt[t], 1u);
+      sm.fsrt[k] = sm.freg[i];
+      sm.fsrt_slot[k] = (uint8_t)t;
+    }
+  if (rt) {
+    sm.base[tid - 64] = resv;
+    if (rc && resv + rc > a.hcap) atomicExch(a.overflow, 1);
+  } else if (rf) {
+    sm.fbase[tid - 64 - kFsBins] = resv;
+    if (rc && resv + rc > a.bcap) atomicExch(a.overflow, 1);
+  }
+  __syncthreads();
+  // flush: consecutive sorted slots of one tile -> consecutive addresses
+  const uint32_t total = sm.total, smask = (1u << shift) - 1;
+  for (uint32_t i = tid; i < total; i += blockDim.x) {
+    const uint32_t key = sm.srt[i];
+    const uint32_t t = key >> shift;
+    EG_CHECK(t < nb && i >= sm.off[t], "fs flush t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
+    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
+    if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = key & smask;
+  }
+  const uint32_t ft = sm.ftotal;
+  for (uint32_t i = tid; i < ft; i += blockDim.x) {
+    const uint32_t t = sm.fsrt_slot[i];
+    const uint32_t pos = sm.fbase[t] + (i - sm.foff[t]);
+    if (pos < a.bcap) a.far_buckets[(uint64_t)t * a.bcap + pos] = sm.fsrt[i];
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t t = tid; t < ring; t += blockDim.x) sm.fcnt[t] = 0;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kFsThreads, 1) k_scatter_fused(const FusedArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1;
+  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) {
+    sm.cnt[t] = 0;
+    sm.fcnt[t] = 0;
+  }
+  if (tid < 8) {
+    uint32_t v = 0;
+    for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
+    sm.cum[tid] = v;
+  }
+  __syncthreads();
+  const uint32_t WS = a.WS;
+  const uint32_t lim = a.ntiles_w << a.log_s;  // positions past the wave's last tile are dropped
+  const uint64_t gw = (uint64_t)blockIdx.x * kFsWarps + warp;
+  const uint64_t nw = (uint64_t)gridDim.x * kFsWarps;
+  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
+  const uint64_t uo = (a.noct + 3) / 4, us = (a.nml - a.noct + 31) / 32, uf = (nfar + 31) / 32;
+  uint32_t* const myreg = sm.reg + warp * kFsRegion;
+  uint64_t* const myfreg = sm.freg + warp * kFsFar;
+  uint8_t* const myfslot = sm.fslot + warp * kFsFar;
+  uint32_t fill = 0, ffill = 0;  // warp-uniform
+
+  // walk state: warp-uniform phase/unit, per-lane prime and position; the
+  // next unit's raw data (x, y) is prefetched while the current one walks
+  int phase = 0;  // 0 octets, 1 singles, 2 far, 3 done
+  uint64_t u = gw;
+  bool loaded = false, ok = false;
+  uint32_t p = 0, s = 0, s0 = 0, pos = WS, step = 0;
+  uint64_t idx = 0;
+  auto unit_index = [&](int ph, uint64_t uu, uint64_t& ix) -> bool {
+    if (ph == 0) {
+      ix = uu * 4 + (lane >> 3);
+      return ix < a.noct;
+    }
+    if (ph == 1) {
+      ix = a.noct + uu * 32 + lane;
+      return ix < a.nml;
+    }
+    ix = uu * 32 + lane;
+    return ix < nfar;
+  };
+  auto fetch = [&](int ph, uint64_t uu, uint32_t& x, uint32_t& y) {
+    uint64_t ix;
+    x = 0;
+    y = 0;
+    if (!unit_index(ph, uu, ix)) return;
+    if (ph < 2) {
+      x = a.ml_p[ix];
+      y = a.ml_state[ix];
+    } else {
+      const uint64_t e = a.far_in[ix];
+      x = (uint32_t)e;
+      y = (uint32_t)(e >> 32);
+    }
+  };
+  auto units_of = [&](int ph) { return ph == 0 ? uo : ph == 1 ? us : uf; };
+  // prefetched next unit
+  int nph = 0;
+  uint64_t nu = gw;
+  while (nph < 3 && nu >= units_of(nph)) {
+    ++nph;
+    nu = gw;
+  }
+  uint32_t nx = 0, ny = 0;
+  if (nph < 3) fetch(nph, nu, nx, ny);
+
+  for (;;) {
+    while (phase < 3 && fill + 32 <= (uint32_t)kFsRegion && ffill + 32 <= (uint32_t)kFsFar) {
+      if (!loaded) {
+        if (nph >= 3) {
+          phase = 3;
+          break;
+        }
+        // take the prefetched unit, prefetch the one after it
+        phase = nph;
+        u = nu;
+        const uint32_t x = nx, y = ny;
+        nu = u + nw;
+        while (nph < 3 && nu >= units_of(nph)) {
+          ++nph;
+          nu = gw;
+        }
+        if (nph < 3) fetch(nph, nu, nx, ny);
+        ok = unit_index(phase, u, idx);
+        p = x;
+        if (phase == 0) {
+          s0 = y >> 29;
+          pos = ok ? (y & 0x1fffffffu) + p * nib(sm.cum[s0], lane & 7) : WS;
+          step = 15u * p;
+        } else if (phase == 1) {
+          pos = ok ? (y & 0x1fffffffu) : WS;
+          s = y >> 29;
+        } else {
+          pos = ok ? (y & 0x1fffffffu) : WS;
+          s = y >> 29;
+        }
+        loaded = true;
+      }
+      const bool v = pos < WS;
+      if (__any_sync(kFull, v)) {
+        const bool emit = v && pos < lim;
+        const uint32_t m = __ballot_sync(kFull, emit);
+        if (emit) myreg[fill + __popc(m & lt)] = pos;
+        fill += __popc(m);
+        if (phase == 0) {
+          if (v) pos += step;
+        } else if (phase == 1) {
+          if (v) {
+            pos += wheel_D(s) * p;
+            s = (s + 1) & 7;
+          }
+        } else {
+          // far: its one hit is staged; the entry moves to the wave of its next hit
+          bool keep = false;
+          uint64_t ne = 0;
+          uint32_t slot = 0;
+          if (v) {
+            const uint64_t q2 = (uint64_t)pos + (uint64_t)wheel_D(s) * p;
+            uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
+            while (d * WS > q2) --d;
+            while ((d + 1) * WS <= q2) ++d;
+            const uint64_t tgt = a.wave + d;
+            if (tgt < a.nwaves) {
+              keep = true;
+              slot = (uint32_t)tgt % a.ring;
+              ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
+            }
+          }
+          const uint32_t fm = __ballot_sync(kFull, keep);
+          if (keep) {
+            const uint32_t k = ffill + __popc(fm & lt);
+            myfreg[k] = ne;
+            myfslot[k] = (uint8_t)slot;
+          }
+          ffill += __popc(fm);
+          pos = WS;
+        }
+      } else {
+        // unit finished: write back the state
+        if (phase == 0) {
+          const uint32_t ex = pos - WS;
+          uint32_t mn = ex;
+          mn = min(mn, __shfl_xor_sync(kFull, mn, 1));
+          mn = min(mn, __shfl_xor_sync(kFull, mn, 2));
+          mn = min(mn, __shfl_xor_sync(kFull, mn, 4));
+          const uint32_t bal = (__ballot_sync(kFull, ex == mn) >> (lane & ~7u)) & 0xffu;
+          if (ok && (lane & 7) == 0) a.ml_state[idx] = mn | (((s0 + __ffs(bal) - 1) & 7) << 29);
+        } else if (phase == 1) {
+          if (ok) a.ml_state[idx] = (pos - WS) | (s << 29);
+        }
+        loaded = false;
+      }
+    }
+    if (lane == 0) {
+      sm.fill[warp] = fill;
+      sm.ffill[warp] = ffill;
+    }
+    const int more = __syncthreads_or(phase < 3);
+    fs_flush(sm, a);
+    fill = 0;
+    ffill = 0;
+    if (!more) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Base primes: odd primes < 2^16 in one CTA (sieve in smem + block compaction).
 __global__ void __launch_bounds__(1024) k_small_primes(uint32_t* __restrict__ out, uint32_t* __restrict__ count) {
   __shared__ uint32_t bits[1024];  // 32768 odd numbers 1..65535
