@@ -11,6 +11,8 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SO = os.path.join(PKG, "liberato_gpu.so")
+CLI = os.path.join(PKG, "erato-gpu")
+CLI_SRC = os.path.join(PKG, "csrc", "erato_cli.cpp")
 SOURCES = [os.path.join(PKG, "csrc", "erato_gpu.cu")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", "sieve_kernels.cuh"), os.path.join(ROOT, "include", "erato_gpu.h")]
 NVCC_FLAGS = [
@@ -34,14 +36,26 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
+def build_cli(verbose: bool = False) -> str:
+    """erato-gpu: the reference CLI contract (tools/erato.cpp) over liberato_gpu.so."""
+    cmd = ["g++", "-O2", "-std=c++17", CLI_SRC, "-o", CLI, f"-L{PKG}", "-lerato_gpu", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     so = SO.replace(".so", "_debug.so") if debug else SO
-    if not force and not debug and up_to_date():
+    if not force and not debug and up_to_date() and os.path.exists(CLI) \
+            and os.path.getmtime(CLI) >= os.path.getmtime(CLI_SRC):
         return SO
     cmd = [nvcc(), *NVCC_FLAGS, *(["-DEG_DEBUG"] if debug else []), "-o", so, *SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
+    if not debug:
+        build_cli(verbose)
     return so
 
 
