@@ -345,13 +345,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
             mark(tile, q + o6);
             mark(tile, q + o7);
           }
-          if (q < S) mark(tile, q);
-          if (q + o1 < S) mark(tile, q + o1);
-          if (q + o2 < S) mark(tile, q + o2);
-          if (q + o3 < S) mark(tile, q + o3);
-          if (q + o4 < S) mark(tile, q + o4);
-          if (q + o5 < S) mark(tile, q + o5);
-          if (q + o6 < S) mark(tile, q + o6);
+          // last partial period: a short wheel walk from class s
+          while (q < S) {
+            mark(tile, q);
+            q += wheel_D(s) * p;
+            s = (s + 1) & 7;
+          }
         }
       }
     }
