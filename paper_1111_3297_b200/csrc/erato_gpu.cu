@@ -544,12 +544,19 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
-    // large-prime path: k_gen + k_bin (default), or the experimental fused
-    // walk+sort kernel (ERATO_GPU_SCATTER=fused; measured 1.5x slower on B200)
+    // large-prime path: the fused walk+sort kernel (default), or k_gen + k_bin
+    // (ERATO_GPU_SCATTER=genbin; the fused kernel is ~1.8x faster at cfg5)
     const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
-    const bool fused = sc_env && std::strcmp(sc_env, "fused") == 0 && ring <= (uint32_t)eg::kFsBins &&
+    const bool fused = !(sc_env && std::strcmp(sc_env, "genbin") == 0) && ring <= (uint32_t)eg::kFsBins &&
                        P.W <= (uint32_t)eg::kFsBins;
     eg::FusedArgs fa{};
+    uint32_t fused_blocks = c->nsm;
+    if (fused) {
+      int occ = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_fused, eg::kFsThreads,
+                                                             sizeof(eg::FusedSmem)));
+      fused_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
+    }
     if (have_large) {
       fa.ml_p = ga.ml_p;
       fa.ml_state = ga.ml_state;
@@ -593,7 +600,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
           fa.ntiles_w = ntw;
           fa.far_in = ga.far_in;
           fa.far_in_count = ga.far_in_count;
-          eg::k_scatter_fused<<<c->nsm, eg::kFsThreads, sizeof(eg::FusedSmem), st>>>(fa);
+          eg::k_scatter_fused<<<fused_blocks, eg::kFsThreads, sizeof(eg::FusedSmem), st>>>(fa);
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           launches += 1;
         } else {

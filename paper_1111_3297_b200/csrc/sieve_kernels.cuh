@@ -902,10 +902,20 @@ struct FusedArgs {
   int* overflow;
 };
 
-constexpr int kFsThreads = 1024;
+#ifndef EG_FS_THREADS
+#define EG_FS_THREADS 256  // measured best on B200 with 640-record regions (4 CTAs/SM)
+#endif
+#ifndef EG_FS_REGION
+#define EG_FS_REGION 640
+#endif
+constexpr int kFsThreads = EG_FS_THREADS;
 constexpr int kFsWarps = kFsThreads / 32;
-constexpr int kFsRegion = 640;  // staged records per warp
-constexpr int kFsFar = 64;      // staged re-bucketed far entries per warp
+static_assert(kFsThreads >= 128, "fs_flush needs two scanning warps plus reservation threads");
+constexpr int kFsRegion = EG_FS_REGION;  // staged records per warp
+#ifndef EG_FS_FAR
+#define EG_FS_FAR 64  // larger far staging costs occupancy (measured slower)
+#endif
+constexpr int kFsFar = EG_FS_FAR;  // staged re-bucketed far entries per warp
 constexpr int kFsBins = 256;    // >= tiles per wave and >= ring slots
 
 struct FusedSmem {
@@ -926,11 +936,16 @@ struct FusedSmem {
 __device__ void fs_flush(FusedSmem& sm, const FusedArgs& a) {
   const uint32_t tid = threadIdx.x, nb = a.ntiles_w, shift = a.log_s, ring = a.ring;
   constexpr uint32_t R = kFsRegion, F = kFsFar;
-  // count
-  for (uint32_t i = tid; i < kFsWarps * R; i += blockDim.x)
-    if (i % R < sm.fill[i / R]) atomicAdd(&sm.cnt[sm.reg[i] >> shift], 1u);
-  for (uint32_t i = tid; i < kFsWarps * F; i += blockDim.x)
-    if (i % F < sm.ffill[i / F]) atomicAdd(&sm.fcnt[sm.fslot[i]], 1u);
+  // count: each warp walks its own region's filled slots
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  {
+    const uint32_t* rg = sm.reg + warp * R;
+    const uint32_t n = sm.fill[warp];
+    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&sm.cnt[rg[i] >> shift], 1u);
+    const uint8_t* fs = sm.fslot + warp * F;
+    const uint32_t fn = sm.ffill[warp];
+    for (uint32_t i = lane; i < fn; i += 32) atomicAdd(&sm.fcnt[fs[i]], 1u);
+  }
   __syncthreads();
   if (tid < 32) {
     const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
@@ -939,41 +954,47 @@ __device__ void fs_flush(FusedSmem& sm, const FusedArgs& a) {
     const uint32_t tot = warp_excl_scan(sm.fcnt, sm.foff, ring);
     if (tid == 32) sm.ftotal = tot;
   }
-  // global reservations, in flight during the placement
-  uint32_t resv = 0, rc = 0;
-  const bool rt = tid >= 64 && tid < 64 + nb;
-  const bool rf = tid >= 64 + kFsBins && tid < 64 + kFsBins + ring;
-  if (rt) {
-    rc = sm.cnt[tid - 64];
-    if (rc) resv = atomicAdd(&a.hitcnt[tid - 64], rc);
-  } else if (rf) {
-    rc = sm.fcnt[tid - 64 - kFsBins];
-    if (rc) resv = atomicAdd(&a.far_bcount[tid - 64 - kFsBins], rc);
+  // global reservations: one atomicAdd per non-empty tile / ring slot,
+  // strided over the threads outside the two scanning warps
+  if (tid >= 64) {
+    for (uint32_t b = tid - 64; b < nb + ring; b += blockDim.x - 64) {
+      if (b < nb) {
+        const uint32_t c = sm.cnt[b];
+        if (c) {
+          const uint32_t r = atomicAdd(&a.hitcnt[b], c);
+          sm.base[b] = r;
+          if (r + c > a.hcap) atomicExch(a.overflow, 1);
+        }
+      } else {
+        const uint32_t t = b - nb, c = sm.fcnt[t];
+        if (c) {
+          const uint32_t r = atomicAdd(&a.far_bcount[t], c);
+          sm.fbase[t] = r;
+          if (r + c > a.bcap) atomicExch(a.overflow, 1);
+        }
+      }
+    }
   }
   __syncthreads();
   for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
   for (uint32_t t = tid; t < ring; t += blockDim.x) sm.fcnt[t] = 0;
   __syncthreads();
   // place
-  for (uint32_t i = tid; i < kFsWarps * R; i += blockDim.x)
-    if (i % R < sm.fill[i / R]) {
-      const uint32_t key = sm.reg[i];
+  {
+    const uint32_t* rg = sm.reg + warp * R;
+    const uint32_t n = sm.fill[warp];
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t key = rg[i];
       const uint32_t t = key >> shift;
       sm.srt[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
     }
-  for (uint32_t i = tid; i < kFsWarps * F; i += blockDim.x)
-    if (i % F < sm.ffill[i / F]) {
-      const uint32_t t = sm.fslot[i];
+    const uint32_t fn = sm.ffill[warp];
+    for (uint32_t i = lane; i < fn; i += 32) {
+      const uint32_t t = sm.fslot[warp * F + i];
       const uint32_t k = sm.foff[t] + atomicAdd(&sm.fcnt[t], 1u);
-      sm.fsrt[k] = sm.freg[i];
+      sm.fsrt[k] = sm.freg[warp * F + i];
       sm.fsrt_slot[k] = (uint8_t)t;
     }
-  if (rt) {
-    sm.base[tid - 64] = resv;
-    if (rc && resv + rc > a.hcap) atomicExch(a.overflow, 1);
-  } else if (rf) {
-    sm.fbase[tid - 64 - kFsBins] = resv;
-    if (rc && resv + rc > a.bcap) atomicExch(a.overflow, 1);
   }
   __syncthreads();
   // flush: consecutive sorted slots of one tile -> consecutive addresses
@@ -997,7 +1018,7 @@ __device__ void fs_flush(FusedSmem& sm, const FusedArgs& a) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kFsThreads, 1) k_scatter_fused(const FusedArgs a) {
+__global__ void __launch_bounds__(kFsThreads) k_scatter_fused(const FusedArgs a) {
   extern __shared__ uint4 smem_raw[];
   FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1023,135 +1044,126 @@ __global__ void __launch_bounds__(kFsThreads, 1) k_scatter_fused(const FusedArgs
   uint8_t* const myfslot = sm.fslot + warp * kFsFar;
   uint32_t fill = 0, ffill = 0;  // warp-uniform
 
-  // walk state: warp-uniform phase/unit, per-lane prime and position; the
-  // next unit's raw data (x, y) is prefetched while the current one walks
+  // Units are walked whole; a warp pauses between units once its region
+  // could not take a worst-case unit (octet: 4 primes x 80 admissible hits
+  // per wave for W <= 150; single: 32 x 8; far: 32 records + 32 entries).
+  constexpr uint32_t kUnitMax = 320;
   int phase = 0;  // 0 octets, 1 singles, 2 far, 3 done
   uint64_t u = gw;
-  bool loaded = false, ok = false;
-  uint32_t p = 0, s = 0, s0 = 0, pos = WS, step = 0;
-  uint64_t idx = 0;
-  auto unit_index = [&](int ph, uint64_t uu, uint64_t& ix) -> bool {
-    if (ph == 0) {
-      ix = uu * 4 + (lane >> 3);
-      return ix < a.noct;
-    }
-    if (ph == 1) {
-      ix = a.noct + uu * 32 + lane;
-      return ix < a.nml;
-    }
-    ix = uu * 32 + lane;
-    return ix < nfar;
-  };
+  auto units_of = [&](int ph) { return ph == 0 ? uo : ph == 1 ? us : uf; };
+  while (phase < 3 && u >= units_of(phase)) {
+    ++phase;
+    u = gw;
+  }
+  // prefetched raw data of the next unit
   auto fetch = [&](int ph, uint64_t uu, uint32_t& x, uint32_t& y) {
-    uint64_t ix;
     x = 0;
     y = 0;
-    if (!unit_index(ph, uu, ix)) return;
-    if (ph < 2) {
-      x = a.ml_p[ix];
-      y = a.ml_state[ix];
-    } else {
-      const uint64_t e = a.far_in[ix];
-      x = (uint32_t)e;
-      y = (uint32_t)(e >> 32);
+    if (ph == 0) {
+      const uint64_t ix = uu * 4 + (lane >> 3);
+      if (ix < a.noct) {
+        x = a.ml_p[ix];
+        y = a.ml_state[ix];
+      }
+    } else if (ph == 1) {
+      const uint64_t ix = a.noct + uu * 32 + lane;
+      if (ix < a.nml) {
+        x = a.ml_p[ix];
+        y = a.ml_state[ix];
+      }
+    } else if (ph == 2) {
+      const uint64_t ix = uu * 32 + lane;
+      if (ix < nfar) {
+        const uint64_t e = a.far_in[ix];
+        x = (uint32_t)e;
+        y = (uint32_t)(e >> 32);
+      }
     }
   };
-  auto units_of = [&](int ph) { return ph == 0 ? uo : ph == 1 ? us : uf; };
-  // prefetched next unit
-  int nph = 0;
-  uint64_t nu = gw;
-  while (nph < 3 && nu >= units_of(nph)) {
-    ++nph;
-    nu = gw;
-  }
   uint32_t nx = 0, ny = 0;
-  if (nph < 3) fetch(nph, nu, nx, ny);
+  if (phase < 3) fetch(phase, u, nx, ny);
 
   for (;;) {
-    while (phase < 3 && fill + 32 <= (uint32_t)kFsRegion && ffill + 32 <= (uint32_t)kFsFar) {
-      if (!loaded) {
-        if (nph >= 3) {
-          phase = 3;
-          break;
-        }
-        // take the prefetched unit, prefetch the one after it
-        phase = nph;
-        u = nu;
-        const uint32_t x = nx, y = ny;
-        nu = u + nw;
-        while (nph < 3 && nu >= units_of(nph)) {
-          ++nph;
-          nu = gw;
-        }
-        if (nph < 3) fetch(nph, nu, nx, ny);
-        ok = unit_index(phase, u, idx);
-        p = x;
-        if (phase == 0) {
-          s0 = y >> 29;
-          pos = ok ? (y & 0x1fffffffu) + p * nib(sm.cum[s0], lane & 7) : WS;
-          step = 15u * p;
-        } else if (phase == 1) {
-          pos = ok ? (y & 0x1fffffffu) : WS;
-          s = y >> 29;
-        } else {
-          pos = ok ? (y & 0x1fffffffu) : WS;
-          s = y >> 29;
-        }
-        loaded = true;
+    while (phase < 3 && fill + kUnitMax <= (uint32_t)kFsRegion && ffill + 32 <= (uint32_t)kFsFar) {
+      const int ph = phase;
+      const uint64_t cu = u;
+      const uint32_t x = nx, y = ny;
+      // advance to the next unit and prefetch it
+      u += nw;
+      while (phase < 3 && u >= units_of(phase)) {
+        ++phase;
+        u = gw;
       }
-      const bool v = pos < WS;
-      if (__any_sync(kFull, v)) {
-        const bool emit = v && pos < lim;
-        const uint32_t m = __ballot_sync(kFull, emit);
-        if (emit) myreg[fill + __popc(m & lt)] = pos;
-        fill += __popc(m);
-        if (phase == 0) {
+      if (phase < 3) fetch(phase, u, nx, ny);
+      if (ph == 0) {
+        const uint64_t idx = cu * 4 + (lane >> 3);
+        const bool ok = idx < a.noct;
+        const uint32_t p = x, s0 = y >> 29;
+        uint32_t pos = ok ? (y & 0x1fffffffu) + p * nib(sm.cum[s0], lane & 7) : WS;
+        const uint32_t step = 15u * p;
+        while (__any_sync(kFull, pos < WS)) {
+          const bool v = pos < WS;
+          const bool emit = v && pos < lim;
+          const uint32_t m = __ballot_sync(kFull, emit);
+          if (emit) myreg[fill + __popc(m & lt)] = pos;
+          fill += __popc(m);
           if (v) pos += step;
-        } else if (phase == 1) {
+        }
+        const uint32_t ex = pos - WS;
+        uint32_t mn = ex;
+        mn = min(mn, __shfl_xor_sync(kFull, mn, 1));
+        mn = min(mn, __shfl_xor_sync(kFull, mn, 2));
+        mn = min(mn, __shfl_xor_sync(kFull, mn, 4));
+        const uint32_t bal = (__ballot_sync(kFull, ex == mn) >> (lane & ~7u)) & 0xffu;
+        if (ok && (lane & 7) == 0) a.ml_state[idx] = mn | (((s0 + __ffs(bal) - 1) & 7) << 29);
+      } else if (ph == 1) {
+        const uint64_t idx = a.noct + cu * 32 + lane;
+        const bool ok = idx < a.nml;
+        const uint32_t p = x;
+        uint32_t pos = ok ? (y & 0x1fffffffu) : WS, s = y >> 29;
+        while (__any_sync(kFull, pos < WS)) {
+          const bool v = pos < WS;
+          const bool emit = v && pos < lim;
+          const uint32_t m = __ballot_sync(kFull, emit);
+          if (emit) myreg[fill + __popc(m & lt)] = pos;
+          fill += __popc(m);
           if (v) {
             pos += wheel_D(s) * p;
             s = (s + 1) & 7;
           }
-        } else {
-          // far: its one hit is staged; the entry moves to the wave of its next hit
-          bool keep = false;
-          uint64_t ne = 0;
-          uint32_t slot = 0;
-          if (v) {
-            const uint64_t q2 = (uint64_t)pos + (uint64_t)wheel_D(s) * p;
-            uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
-            while (d * WS > q2) --d;
-            while ((d + 1) * WS <= q2) ++d;
-            const uint64_t tgt = a.wave + d;
-            if (tgt < a.nwaves) {
-              keep = true;
-              slot = (uint32_t)tgt % a.ring;
-              ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
-            }
-          }
-          const uint32_t fm = __ballot_sync(kFull, keep);
-          if (keep) {
-            const uint32_t k = ffill + __popc(fm & lt);
-            myfreg[k] = ne;
-            myfslot[k] = (uint8_t)slot;
-          }
-          ffill += __popc(fm);
-          pos = WS;
         }
+        if (ok) a.ml_state[idx] = (pos - WS) | (s << 29);
       } else {
-        // unit finished: write back the state
-        if (phase == 0) {
-          const uint32_t ex = pos - WS;
-          uint32_t mn = ex;
-          mn = min(mn, __shfl_xor_sync(kFull, mn, 1));
-          mn = min(mn, __shfl_xor_sync(kFull, mn, 2));
-          mn = min(mn, __shfl_xor_sync(kFull, mn, 4));
-          const uint32_t bal = (__ballot_sync(kFull, ex == mn) >> (lane & ~7u)) & 0xffu;
-          if (ok && (lane & 7) == 0) a.ml_state[idx] = mn | (((s0 + __ffs(bal) - 1) & 7) << 29);
-        } else if (phase == 1) {
-          if (ok) a.ml_state[idx] = (pos - WS) | (s << 29);
+        const uint64_t idx = cu * 32 + lane;
+        const bool ok = idx < nfar;
+        const uint32_t p = x, q = y & 0x1fffffffu, s = y >> 29;
+        const bool emit = ok && q < lim;
+        const uint32_t m = __ballot_sync(kFull, emit);
+        if (emit) myreg[fill + __popc(m & lt)] = q;
+        fill += __popc(m);
+        // the entry moves to the wave of its next hit (Lemma 2)
+        bool keep = false;
+        uint64_t ne = 0;
+        uint32_t slot = 0;
+        if (ok) {
+          const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
+          uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
+          while (d * WS > q2) --d;
+          while ((d + 1) * WS <= q2) ++d;
+          const uint64_t tgt = a.wave + d;
+          if (tgt < a.nwaves) {
+            keep = true;
+            slot = (uint32_t)tgt % a.ring;
+            ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
+          }
         }
-        loaded = false;
+        const uint32_t fm = __ballot_sync(kFull, keep);
+        if (keep) {
+          const uint32_t k = ffill + __popc(fm & lt);
+          myfreg[k] = ne;
+          myfslot[k] = (uint8_t)slot;
+        }
+        ffill += __popc(fm);
       }
     }
     if (lane == 0) {
