@@ -57,9 +57,11 @@ ROOF = {
 # Hit records of large primes in this implementation (mod-30 wheel, 2^20-bit
 # tiles), tools/roofline_counts.py `ours_large_records`: k_bin moves 8 B per record.
 LARGE_RECORDS = {1: 0, 2: 0, 3: 20_188, 4: 835_065_655, 5: 7_429_219_143}
+# ... of which come from far primes (p > WS = 146 tiles), `ours_far_records`
+FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_802_335_964}
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # (profiles/r01_ncu_summary.txt, cfg5 wave 100)
-NCU_TRAFFIC = {5: {"k_bin": 206.2e6 + 153.1e6, "k_gen": 132.9e6 + 186.5e6, "k_tile": 133.8e6 + 3.9e6}}
+NCU_TRAFFIC = {5: {"k_scatter_fused": 132.5e6 + 178.7e6, "k_bin": 206.2e6 + 153.1e6, "k_gen": 132.9e6 + 186.5e6, "k_tile": 133.8e6 + 4.5e6}}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 R_ATOM_MEASURED = 3.47e12  # smem atomicOr/s per B200, microbench/mb_atomics.cu (profiles/r01_microbench_atomics.log)
 
@@ -253,12 +255,16 @@ def run_ours(args):
     t_atom = A / R_ATOM_MEASURED
     bound = "hbm" if t_hbm >= t_atom else "atomic"
     achieved_gbs = B / (ms / 1e3) / 1e9 / world  # per GPU, each GPU does 1/world of B
-    # dominant kernel (largest device time in the phase-timed pass); the
-    # default large-prime path is one fused kernel (its time lands in gen_s)
-    fused = os.environ.get("ERATO_GPU_SCATTER", "fused") != "genbin"
-    split = {"k_tile": ph.small_s, "k_gen": ph.gen_s, "k_bin": ph.bin_s}
-    if fused:
+    # dominant kernel (largest device time in the phase-timed pass).  Default
+    # large-prime path: k_scatter_ml (time in gen_s) + k_scatter_far (bin_s);
+    # ERATO_GPU_SCATTER=fused: one kernel; =genbin: k_gen + k_bin
+    mode = os.environ.get("ERATO_GPU_SCATTER", "split")
+    if mode == "genbin":
+        split = {"k_tile": ph.small_s, "k_gen": ph.gen_s, "k_bin": ph.bin_s}
+    elif mode == "fused":
         split = {"k_tile": ph.small_s, "k_scatter_fused": ph.gen_s + ph.bin_s}
+    else:
+        split = {"k_tile": ph.small_s, "k_scatter_ml": ph.gen_s, "k_scatter_far": ph.bin_s}
     dom = max(split, key=split.get)
     waves = max(ph.waves, 1)
     recs = LARGE_RECORDS[args.config] / world
@@ -266,6 +272,9 @@ def run_ours(args):
         "k_bin": 8.0 * recs / waves,                                   # read + write each record
         "k_gen": (4.0 * recs + 8.0 * ph.base_primes) / waves,          # records out + prime state
         "k_scatter_fused": (4.0 * recs + 8.0 * ph.base_primes) / waves,  # sorted records out + prime state
+        # ML: records out + prime state read/write; far: record out + entry in + entry out
+        "k_scatter_ml": (4.0 * (recs - FAR_RECORDS[args.config] / world) + 8.0 * ph.base_primes) / waves,
+        "k_scatter_far": 20.0 * FAR_RECORDS[args.config] / world / waves,
         "k_tile": (params.table_bytes() + 4.0 * recs) / waves,         # table out + records in
     }
     launch_s = split[dom] / waves

@@ -245,6 +245,10 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
                                 (int)sizeof(eg::BinSmem)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::FusedSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_ml, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(eg::MlSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_far, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(eg::FarSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure(8192 * 16));
@@ -438,7 +442,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
       CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 4));
-      CUDA_TRY(c->hits.ensure((uint64_t)P.W * hcap * 4));
+      CUDA_TRY(c->hits.ensure(((uint64_t)P.W * hcap + eg::kScTrash) * 4));  // + trash of the split scatter
       CUDA_TRY(c->hitcnt.ensure((uint64_t)P.W * 4));
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
       if (nfar) {
@@ -448,7 +452,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
         bcap = (uint32_t)std::min<double>((eb * 1.10 + 8192) * c->bcap_scale, (double)nfar + 64);
       }
-      CUDA_TRY(c->buckets.ensure((uint64_t)ring * bcap * 8));
+      CUDA_TRY(c->buckets.ensure(((uint64_t)ring * bcap + eg::kScTrash) * 8));
       {
         const uint64_t gen_warps = (uint64_t)c->nsm * kGenBlocksPerSm * (eg::kGenThreads / 32);
         const double per_wave = eh * P.W;  // records per wave
@@ -544,18 +548,34 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
-    // large-prime path: the fused walk+sort kernel (default), or k_gen + k_bin
-    // (ERATO_GPU_SCATTER=genbin; the fused kernel is ~1.8x faster at cfg5)
+    // large-prime path: k_scatter_ml + k_scatter_far (default), the single
+    // fused walk+sort kernel (ERATO_GPU_SCATTER=fused, or when 32-bit list
+    // offsets do not fit), or k_gen + k_bin (=genbin, or > 256 bins)
     const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
-    const bool fused = !(sc_env && std::strcmp(sc_env, "genbin") == 0) && ring <= (uint32_t)eg::kFsBins &&
-                       P.W <= (uint32_t)eg::kFsBins;
+    const bool sortable = ring <= (uint32_t)eg::kFsBins && P.W <= (uint32_t)eg::kFsBins;
+    const bool genbin = (sc_env && std::strcmp(sc_env, "genbin") == 0) || !sortable;
+    bool fused = !genbin && sc_env && std::strcmp(sc_env, "fused") == 0;
+    // the split kernels index lists and buckets with 32-bit offsets
+    const bool idx32 = (uint64_t)P.W * hcap + eg::kScTrash < (1ull << 32) &&
+                       (uint64_t)ring * bcap + eg::kScTrash < (1ull << 32);
+    const bool split = !genbin && !fused && idx32;
+    if (!genbin && !split) fused = true;
     eg::FusedArgs fa{};
-    uint32_t fused_blocks = c->nsm;
+    uint32_t fused_blocks = c->nsm, ml_blocks = c->nsm, far_blocks = c->nsm;
     if (fused) {
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_fused, eg::kFsThreads,
                                                              sizeof(eg::FusedSmem)));
       fused_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
+    }
+    if (split) {
+      int occ = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml, eg::kMlWarps * 32,
+                                                             sizeof(eg::MlSmem)));
+      ml_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_far, eg::kFarWarps * 32,
+                                                             sizeof(eg::FarSmem)));
+      far_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
     }
     if (have_large) {
       fa.ml_p = ga.ml_p;
@@ -595,7 +615,25 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-        if (fused) {
+        if (split) {
+          fa.wave = w;
+          fa.ntiles_w = ntw;
+          fa.far_in = ga.far_in;
+          fa.far_in_count = ga.far_in_count;
+          if (nml) {
+            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(fa);
+            launches += 1;
+          }
+          if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
+          if (nfar) {
+            eg::FarArgs far{};
+            far.f = fa;
+            far.wslot = slot;
+            far.inv_ws_f = 1.0f / (float)P.WS;
+            eg::k_scatter_far<<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(far);
+            launches += 1;
+          }
+        } else if (fused) {
           fa.wave = w;
           fa.ntiles_w = ntw;
           fa.far_in = ga.far_in;

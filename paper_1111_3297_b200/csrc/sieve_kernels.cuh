@@ -1179,6 +1179,309 @@ __global__ void __launch_bounds__(kFsThreads) k_scatter_fused(const FusedArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// Split large-prime path: k_scatter_ml walks the ML primes (S < p <= WS),
+// k_scatter_far the far bucket of the wave.  Same staging/sort/flush scheme as
+// k_scatter_fused, but each kernel has one kind of unit, so
+//  * the ML walk is resumable per step (one lane per prime, all ML primes):
+//    a warp walks until its region is full, not until a unit ends, and every
+//    round flushes nearly full regions;
+//  * the far kernel sizes its staging for far entries (one per lane per
+//    unit), so far rounds are ~8x rarer than with 64-entry staging;
+//  * no phase machine, and the far next-wave index is an fp32 estimate plus
+//    an exact 32-bit wrap-around correction instead of fp64 + u64 division.
+template <int NW, int R, int F>
+struct ScSmem {
+  static constexpr int FF = F > 0 ? F : 1;
+  uint32_t reg[NW * R];  // staged records, warp w at [w * R]
+  uint32_t srt[NW * R];  // sorted by tile
+  uint64_t freg[NW * FF];
+  uint64_t fsrt[NW * FF];
+  uint8_t fslot[NW * FF];
+  uint8_t fsrt_slot[NW * FF];
+  uint32_t fill[NW], ffill[NW];
+  // cnt: per-round counts (bumped at emission), then placement cursors;
+  // gofs[t] = global index of sorted slot 0 of bin t (t*cap + reserved - off)
+  uint32_t cnt[kFsBins], off[kFsBins], gofs[kFsBins];
+  uint32_t fcnt[kFsBins], foff[kFsBins], fgofs[kFsBins];
+  uint32_t total, ftotal;
+};
+
+// Round of the split scatter kernels: the staged records of every warp were
+// already counted per tile (far entries per ring slot) while they were
+// emitted.  Scan, one global reservation per non-empty bin, placement into
+// tile order, coalesced flush.  A bin whose reservation overflows its list
+// is redirected to the trash area past the lists (the host retries the run
+// with larger lists when the overflow flag is set).
+template <int NW, int R, int F>
+__device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nb = a.ntiles_w, shift = a.log_s, ring = F > 0 ? a.ring : 0;
+  constexpr uint32_t NT = NW * 32, FF = ScSmem<NW, R, F>::FF;
+  constexpr uint32_t kScan = F > 0 ? 64 : 32;  // scanning threads
+  // (the caller's barrier orders the emission-time counts before the scan)
+  if (tid < 32) {
+    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
+    if (tid == 0) sm.total = tot;
+  } else if (F > 0 && tid < 64) {
+    const uint32_t tot = warp_excl_scan(sm.fcnt, sm.foff, ring);
+    if (tid == 32) sm.ftotal = tot;
+  } else {
+    for (uint32_t b = tid - kScan; b < nb + ring; b += NT - kScan) {
+      if (b < nb) {
+        const uint32_t c = sm.cnt[b];
+        if (c) {
+          const uint32_t r = atomicAdd(&a.hitcnt[b], c);
+          const bool over = r + c > a.hcap;
+          if (over) atomicExch(a.overflow, 1);
+          sm.gofs[b] = over ? 0xffffffffu : b * a.hcap + r;
+        }
+      } else {
+        const uint32_t t = b - nb, c = sm.fcnt[t];
+        if (c) {
+          const uint32_t r = atomicAdd(&a.far_bcount[t], c);
+          const bool over = r + c > a.bcap;
+          if (over) atomicExch(a.overflow, 1);
+          sm.fgofs[t] = over ? 0xffffffffu : t * a.bcap + r;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // cursors and final offsets
+  const uint32_t trash = nb * a.hcap;  // the hit lists of this wave end here
+  for (uint32_t t = tid; t < nb; t += NT) {
+    const uint32_t o = sm.off[t];
+    const uint32_t g = sm.gofs[t];
+    if (sm.cnt[t]) sm.gofs[t] = (g == 0xffffffffu ? trash : g) - o;
+    sm.cnt[t] = o;
+  }
+  if constexpr (F > 0) {
+    const uint32_t ftrash = a.ring * a.bcap;
+    for (uint32_t t = tid; t < ring; t += NT) {
+      const uint32_t o = sm.foff[t];
+      const uint32_t g = sm.fgofs[t];
+      if (sm.fcnt[t]) sm.fgofs[t] = (g == 0xffffffffu ? ftrash : g) - o;
+      sm.fcnt[t] = o;
+    }
+  }
+  __syncthreads();
+  {
+    const uint32_t* rg = sm.reg + warp * R;
+    const uint32_t n = sm.fill[warp];
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t key = rg[i];
+      sm.srt[atomicAdd(&sm.cnt[key >> shift], 1u)] = key;
+    }
+    if constexpr (F > 0) {
+      const uint32_t fn = sm.ffill[warp];
+      for (uint32_t i = lane; i < fn; i += 32) {
+        const uint32_t t = sm.fslot[warp * FF + i];
+        const uint32_t k = atomicAdd(&sm.fcnt[t], 1u);
+        sm.fsrt[k] = sm.freg[warp * FF + i];
+        sm.fsrt_slot[k] = (uint8_t)t;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t total = sm.total, smask = (1u << shift) - 1;
+  for (uint32_t i = tid; i < total; i += NT) {
+    const uint32_t key = sm.srt[i];
+    a.hits[sm.gofs[key >> shift] + i] = key & smask;
+  }
+  if constexpr (F > 0) {
+    const uint32_t ft = sm.ftotal;
+    for (uint32_t i = tid; i < ft; i += NT) a.far_buckets[sm.fgofs[sm.fsrt_slot[i]] + i] = sm.fsrt[i];
+  }
+  __syncthreads();
+  for (uint32_t t = tid; t < nb; t += NT) sm.cnt[t] = 0;
+  if constexpr (F > 0)
+    for (uint32_t t = tid; t < ring; t += NT) sm.fcnt[t] = 0;
+  __syncthreads();  // counts are zero before any warp emits again
+}
+
+#ifndef EG_ML_WARPS
+#define EG_ML_WARPS 8
+#endif
+#ifndef EG_ML_REGION
+#define EG_ML_REGION 384
+#endif
+#ifndef EG_FAR_WARPS
+#define EG_FAR_WARPS 8
+#endif
+#ifndef EG_FAR_REGION
+#define EG_FAR_REGION 128
+#endif
+constexpr int kMlWarps = EG_ML_WARPS, kMlRegion = EG_ML_REGION;
+constexpr int kFarWarps = EG_FAR_WARPS, kFarRegion = EG_FAR_REGION;
+using MlSmem = ScSmem<kMlWarps, kMlRegion, 0>;
+using FarSmem = ScSmem<kFarWarps, kFarRegion, kFarRegion>;
+// records one round may send to the trash area (per CTA)
+constexpr uint32_t kScTrash = (uint32_t)(kMlWarps * kMlRegion > kFarWarps * kFarRegion ? kMlWarps * kMlRegion
+                                                                                        : kFarWarps * kFarRegion);
+static_assert(kMlWarps >= 2 && kFarWarps >= 3, "sc_flush needs scanning warps plus reservation threads");
+
+__device__ __forceinline__ uint32_t rotr4(uint32_t x) { return __funnelshift_r(x, x, 4); }
+
+__global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  MlSmem& sm = *reinterpret_cast<MlSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1;
+  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) sm.cnt[t] = 0;
+  __syncthreads();
+  const uint32_t WS = a.WS, shift = a.log_s;
+  // walk bound: the wave end, or the end of the last tile in the last wave
+  // (the state written back after the last wave is never read)
+  const uint32_t B = a.ntiles_w << a.log_s;
+  const uint32_t nw = gridDim.x * kMlWarps;
+  const uint32_t nu = (a.nml + 31) / 32;
+  uint32_t* const myreg = sm.reg + warp * kMlRegion;
+  uint32_t u = blockIdx.x * kMlWarps + warp;
+  uint32_t idx = u * 32 + lane;
+  bool ok = u < nu && idx < a.nml;
+  uint32_t p = ok ? a.ml_p[idx] : 0, y = ok ? a.ml_state[idx] : 0;
+  uint32_t pos = ok ? (y & 0x1fffffffu) : B, s = y >> 29;
+  uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
+  uint32_t nidx = (u + nw) * 32 + lane;
+  uint32_t np = 0, ny = 0;
+  if (u + nw < nu && nidx < a.nml) {
+    np = a.ml_p[nidx];
+    ny = a.ml_state[nidx];
+  }
+  bool live = u < nu;  // warp-uniform
+  uint32_t fill = 0;
+  for (;;) {
+    while (live && fill + 32 <= (uint32_t)kMlRegion) {
+      const bool v = pos < B;
+      const uint32_t m = __ballot_sync(kFull, v);
+      if (m == 0) {
+        if (ok) a.ml_state[idx] = (pos - WS) | ((s & 7) << 29);
+        u += nw;
+        if (u >= nu) {
+          live = false;
+          break;
+        }
+        idx = nidx;
+        ok = idx < a.nml;
+        p = np;
+        pos = ok ? (ny & 0x1fffffffu) : B;
+        s = ny >> 29;
+        dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+        nidx = (u + nw) * 32 + lane;
+        np = 0;
+        ny = 0;
+        if (u + nw < nu && nidx < a.nml) {
+          np = a.ml_p[nidx];
+          ny = a.ml_state[nidx];
+        }
+        continue;
+      }
+      if (v) {
+        myreg[fill + __popc(m & lt)] = pos;
+        atomicAdd(&sm.cnt[pos >> shift], 1u);
+        pos += (dd & 15u) * p;
+        dd = rotr4(dd);
+        ++s;
+      }
+      fill += __popc(m);
+    }
+    if (lane == 0) sm.fill[warp] = fill;
+    const int more = __syncthreads_or(live);
+    sc_flush(sm, a);
+    fill = 0;
+    if (!more) break;
+  }
+}
+
+struct FarArgs {
+  FusedArgs f;
+  uint32_t wslot;   // wave % ring
+  float inv_ws_f;   // 1 / WS
+};
+
+__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa) {
+  extern __shared__ uint4 smem_raw[];
+  FarSmem& sm = *reinterpret_cast<FarSmem*>(smem_raw);
+  const FusedArgs& a = fa.f;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1;
+  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) {
+    sm.cnt[t] = 0;
+    sm.fcnt[t] = 0;
+  }
+  __syncthreads();
+  const uint32_t WS = a.WS, ring = a.ring, shift = a.log_s;
+  const uint32_t lim = a.ntiles_w << a.log_s;
+  const uint32_t nfar = min(*a.far_in_count, a.bcap);
+  const uint32_t nw = gridDim.x * kFarWarps;
+  const uint32_t nu = (nfar + 31) / 32;
+  const uint64_t left = a.nwaves - a.wave;  // waves from this one to the end
+  uint32_t* const myreg = sm.reg + warp * kFarRegion;
+  uint64_t* const myfreg = sm.freg + warp * kFarRegion;
+  uint8_t* const myfslot = sm.fslot + warp * kFarRegion;
+  uint32_t u = blockIdx.x * kFarWarps + warp;
+  uint64_t ne = 0;
+  {
+    const uint32_t i = u * 32 + lane;
+    if (u < nu && i < nfar) ne = a.far_in[i];
+  }
+  uint32_t fill = 0, ffill = 0;
+  for (;;) {
+    while (u < nu && fill + 32 <= (uint32_t)kFarRegion && ffill + 32 <= (uint32_t)kFarRegion) {
+      const uint32_t i = u * 32 + lane;
+      const bool ok = i < nfar;
+      const uint64_t e = ne;
+      u += nw;
+      {
+        const uint32_t j = u * 32 + lane;
+        ne = (u < nu && j < nfar) ? a.far_in[j] : 0;
+      }
+      const uint32_t p = (uint32_t)e, q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
+      const bool emit = ok && q < lim;
+      const uint32_t m = __ballot_sync(kFull, emit);
+      if (emit) {
+        myreg[fill + __popc(m & lt)] = q;
+        atomicAdd(&sm.cnt[q >> shift], 1u);
+      }
+      fill += __popc(m);
+      // next hit q + D*p lies d waves ahead (Lemma 2): fp32 estimate of d,
+      // then the exact remainder in 32-bit wrap-around arithmetic
+      const uint32_t D = wheel_D(s);
+      uint32_t d = __float2uint_rz(__fmaf_rn((float)D, (float)p, (float)q) * fa.inv_ws_f);
+      int32_t r = (int32_t)(q + D * p - d * WS);
+      while (r < 0) {
+        r += (int32_t)WS;
+        --d;
+      }
+      while (r >= (int32_t)WS) {
+        r -= (int32_t)WS;
+        ++d;
+      }
+      const bool keep = ok && d < left;
+      uint32_t slot = fa.wslot + d;
+      if (slot >= ring) slot -= ring;
+      const uint32_t fm = __ballot_sync(kFull, keep);
+      if (keep) {
+        const uint32_t k = ffill + __popc(fm & lt);
+        myfreg[k] = (uint64_t)p | ((uint64_t)((uint32_t)r | (((s + 1) & 7) << 29)) << 32);
+        myfslot[k] = (uint8_t)slot;
+        atomicAdd(&sm.fcnt[slot], 1u);
+      }
+      ffill += __popc(fm);
+    }
+    if (lane == 0) {
+      sm.fill[warp] = fill;
+      sm.ffill[warp] = ffill;
+    }
+    const int more = __syncthreads_or(u < nu);
+    sc_flush(sm, a);
+    fill = 0;
+    ffill = 0;
+    if (!more) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Base primes: odd primes < 2^16 in one CTA (sieve in smem + block compaction).
 __global__ void __launch_bounds__(1024) k_small_primes(uint32_t* __restrict__ out, uint32_t* __restrict__ count) {
   __shared__ uint32_t bits[1024];  // 32768 odd numbers 1..65535

@@ -45,7 +45,7 @@ def odd_upto(x: np.ndarray) -> np.ndarray:
     return (np.maximum(x, 0) + 1) // 2
 
 
-def counts(l: int, f: int, n: int, log_tile: int = 20):
+def counts(l: int, f: int, n: int, log_tile: int = 20, wave_tiles: int = 146):
     R = Restated()
     u = (f << (l + 1)) + 1
     v = (f + n) << (l + 1)
@@ -82,7 +82,10 @@ def counts(l: int, f: int, n: int, log_tile: int = 20):
         "B_bytes": B, "A_atomics": A,
         "ours_medium_marks": int(ours_marks[ours_med].sum()),
         "ours_large_records": int(ours_marks[ours_large].sum()),
+        # far primes (p > WS = wave_tiles * 2^log_tile) reach the wave through the bucket ring
+        "ours_far_records": int(ours_marks[primes > wave_tiles * S].sum()),
         "ours_log_tile": log_tile,
+        "ours_wave_tiles": wave_tiles,
     }
 
 
