@@ -184,6 +184,9 @@ struct TileArgs {
   int p2_floor;                  // 1: multiples from p^2 (overlap runs, base sieve)
 };
 
+#ifndef EG_TILE_DYNAMIC
+#define EG_TILE_DYNAMIC 0
+#endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 4096;  // medium primes below S/64 (1900 at S = 2^20)
 constexpr int kTileWarps = kTileThreads / 32;
@@ -292,11 +295,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       s_wq[i] = make_uint2(q0, p | (s << 29));
     }
     __syncthreads();
+#if EG_TILE_DYNAMIC
     for (;;) {
       uint32_t item = 0;
       if (lane == 0) item = atomicAdd(&s_item, 1u);
       item = __shfl_sync(kFull, item, 0);
       if (item >= a.nmed_warp) break;
+#else
+    // static round-robin (no barrier follows: the lane-per-prime phase
+    // absorbs the imbalance)
+    for (uint32_t item = warp; item < a.nmed_warp; item += kTileWarps) {
+#endif
       const uint2 w = s_wq[item];
       const uint32_t p = w.y & 0x1fffffffu, s = w.y >> 29;
       uint32_t q = w.x + p * (nib(s_cum[s], lane & 7) + 15u * (lane >> 3));
@@ -1342,12 +1351,19 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
   uint32_t p = ok ? a.ml_p[idx] : 0, y = ok ? a.ml_state[idx] : 0;
   uint32_t pos = ok ? (y & 0x1fffffffu) : B, s = y >> 29;
   uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
-  uint32_t nidx = (u + nw) * 32 + lane;
-  uint32_t np = 0, ny = 0;
-  if (u + nw < nu && nidx < a.nml) {
-    np = a.ml_p[nidx];
-    ny = a.ml_state[nidx];
-  }
+  // the next two units' primes and states are in flight
+  auto load = [&](uint32_t uu, uint32_t& xp, uint32_t& xy) {
+    const uint32_t j = uu * 32 + lane;
+    xp = 0;
+    xy = 0;
+    if (uu < nu && j < a.nml) {
+      xp = a.ml_p[j];
+      xy = a.ml_state[j];
+    }
+  };
+  uint32_t np0, ny0, np1, ny1;
+  load(u + nw, np0, ny0);
+  load(u + 2 * nw, np1, ny1);
   bool live = u < nu;  // warp-uniform
   uint32_t fill = 0;
   for (;;) {
@@ -1361,19 +1377,15 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
           live = false;
           break;
         }
-        idx = nidx;
+        idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = np;
-        pos = ok ? (ny & 0x1fffffffu) : B;
-        s = ny >> 29;
+        p = np0;
+        pos = ok ? (ny0 & 0x1fffffffu) : B;
+        s = ny0 >> 29;
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
-        nidx = (u + nw) * 32 + lane;
-        np = 0;
-        ny = 0;
-        if (u + nw < nu && nidx < a.nml) {
-          np = a.ml_p[nidx];
-          ny = a.ml_state[nidx];
-        }
+        np0 = np1;
+        ny0 = ny1;
+        load(u + 2 * nw, np1, ny1);
         continue;
       }
       if (v) {
@@ -1420,22 +1432,21 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
   uint64_t* const myfreg = sm.freg + warp * kFarRegion;
   uint8_t* const myfslot = sm.fslot + warp * kFarRegion;
   uint32_t u = blockIdx.x * kFarWarps + warp;
-  uint64_t ne = 0;
-  {
-    const uint32_t i = u * 32 + lane;
-    if (u < nu && i < nfar) ne = a.far_in[i];
-  }
+  // the entries of the next two units are in flight (loads issued early)
+  auto load = [&](uint32_t uu) -> uint64_t {
+    const uint32_t j = uu * 32 + lane;
+    return (uu < nu && j < nfar) ? a.far_in[j] : 0;
+  };
+  uint64_t ne0 = load(u), ne1 = load(u + nw);
   uint32_t fill = 0, ffill = 0;
   for (;;) {
     while (u < nu && fill + 32 <= (uint32_t)kFarRegion && ffill + 32 <= (uint32_t)kFarRegion) {
       const uint32_t i = u * 32 + lane;
       const bool ok = i < nfar;
-      const uint64_t e = ne;
+      const uint64_t e = ne0;
+      ne0 = ne1;
+      ne1 = load(u + 2 * nw);
       u += nw;
-      {
-        const uint32_t j = u * 32 + lane;
-        ne = (u < nu && j < nfar) ? a.far_in[j] : 0;
-      }
       const uint32_t p = (uint32_t)e, q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
       const bool emit = ok && q < lim;
       const uint32_t m = __ballot_sync(kFull, emit);
