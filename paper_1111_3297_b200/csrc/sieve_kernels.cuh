@@ -1204,15 +1204,15 @@ struct ScSmem {
   uint32_t reg[NW * R];  // staged records, warp w at [w * R]
   uint32_t srt[NW * R];  // sorted by tile
   uint64_t freg[NW * FF];
-  uint64_t fsrt[NW * FF];
+  uint16_t frank[NW * FF];  // rank among this round's entries of the same slot
   uint8_t fslot[NW * FF];
-  uint8_t fsrt_slot[NW * FF];
   uint32_t fill[NW], ffill[NW];
   // cnt: per-round counts (bumped at emission), then placement cursors;
   // gofs[t] = global index of sorted slot 0 of bin t (t*cap + reserved - off)
   uint32_t cnt[kFsBins], off[kFsBins], gofs[kFsBins];
-  uint32_t fcnt[kFsBins], foff[kFsBins], fgofs[kFsBins];
-  uint32_t total, ftotal;
+  uint32_t fcnt[kFsBins], fgofs[kFsBins];
+  uint32_t total;
+  static_assert(NW * FF < 65536, "far ranks are 16-bit");
 };
 
 // Round of the split scatter kernels: the staged records of every warp were
@@ -1226,14 +1226,11 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nb = a.ntiles_w, shift = a.log_s, ring = F > 0 ? a.ring : 0;
   constexpr uint32_t NT = NW * 32, FF = ScSmem<NW, R, F>::FF;
-  constexpr uint32_t kScan = F > 0 ? 64 : 32;  // scanning threads
+  constexpr uint32_t kScan = 32;  // scanning threads
   // (the caller's barrier orders the emission-time counts before the scan)
   if (tid < 32) {
     const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
     if (tid == 0) sm.total = tot;
-  } else if (F > 0 && tid < 64) {
-    const uint32_t tot = warp_excl_scan(sm.fcnt, sm.foff, ring);
-    if (tid == 32) sm.ftotal = tot;
   } else {
     for (uint32_t b = tid - kScan; b < nb + ring; b += NT - kScan) {
       if (b < nb) {
@@ -1265,13 +1262,11 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
     sm.cnt[t] = o;
   }
   if constexpr (F > 0) {
+    // far entries go straight from staging to their bucket run: the
+    // emission-time count returned each entry's rank within (round, slot)
     const uint32_t ftrash = a.ring * a.bcap;
-    for (uint32_t t = tid; t < ring; t += NT) {
-      const uint32_t o = sm.foff[t];
-      const uint32_t g = sm.fgofs[t];
-      if (sm.fcnt[t]) sm.fgofs[t] = (g == 0xffffffffu ? ftrash : g) - o;
-      sm.fcnt[t] = o;
-    }
+    for (uint32_t t = tid; t < ring; t += NT)
+      if (sm.fcnt[t] && sm.fgofs[t] == 0xffffffffu) sm.fgofs[t] = ftrash;
   }
   __syncthreads();
   {
@@ -1284,10 +1279,8 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
     if constexpr (F > 0) {
       const uint32_t fn = sm.ffill[warp];
       for (uint32_t i = lane; i < fn; i += 32) {
-        const uint32_t t = sm.fslot[warp * FF + i];
-        const uint32_t k = atomicAdd(&sm.fcnt[t], 1u);
-        sm.fsrt[k] = sm.freg[warp * FF + i];
-        sm.fsrt_slot[k] = (uint8_t)t;
+        const uint32_t j = warp * FF + i;
+        a.far_buckets[sm.fgofs[sm.fslot[j]] + sm.frank[j]] = sm.freg[j];
       }
     }
   }
@@ -1296,10 +1289,6 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
   for (uint32_t i = tid; i < total; i += NT) {
     const uint32_t key = sm.srt[i];
     a.hits[sm.gofs[key >> shift] + i] = key & smask;
-  }
-  if constexpr (F > 0) {
-    const uint32_t ft = sm.ftotal;
-    for (uint32_t i = tid; i < ft; i += NT) a.far_buckets[sm.fgofs[sm.fsrt_slot[i]] + i] = sm.fsrt[i];
   }
   __syncthreads();
   for (uint32_t t = tid; t < nb; t += NT) sm.cnt[t] = 0;
@@ -1318,7 +1307,7 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
 #define EG_FAR_WARPS 8
 #endif
 #ifndef EG_FAR_REGION
-#define EG_FAR_REGION 128
+#define EG_FAR_REGION 192
 #endif
 constexpr int kMlWarps = EG_ML_WARPS, kMlRegion = EG_ML_REGION;
 constexpr int kFarWarps = EG_FAR_WARPS, kFarRegion = EG_FAR_REGION;
@@ -1431,6 +1420,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
   uint32_t* const myreg = sm.reg + warp * kFarRegion;
   uint64_t* const myfreg = sm.freg + warp * kFarRegion;
   uint8_t* const myfslot = sm.fslot + warp * kFarRegion;
+  uint16_t* const myfrank = sm.frank + warp * kFarRegion;
   uint32_t u = blockIdx.x * kFarWarps + warp;
   // the entries of the next two units are in flight (loads issued early)
   auto load = [&](uint32_t uu) -> uint64_t {
@@ -1476,7 +1466,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
         const uint32_t k = ffill + __popc(fm & lt);
         myfreg[k] = (uint64_t)p | ((uint64_t)((uint32_t)r | (((s + 1) & 7) << 29)) << 32);
         myfslot[k] = (uint8_t)slot;
-        atomicAdd(&sm.fcnt[slot], 1u);
+        myfrank[k] = (uint16_t)atomicAdd(&sm.fcnt[slot], 1u);
       }
       ffill += __popc(fm);
     }
