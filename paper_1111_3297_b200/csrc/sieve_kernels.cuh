@@ -1309,6 +1309,9 @@ __device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
 #ifndef EG_FAR_REGION
 #define EG_FAR_REGION 192
 #endif
+#ifndef EG_ML_PF
+#define EG_ML_PF 1
+#endif
 constexpr int kMlWarps = EG_ML_WARPS, kMlRegion = EG_ML_REGION;
 constexpr int kFarWarps = EG_FAR_WARPS, kFarRegion = EG_FAR_REGION;
 using MlSmem = ScSmem<kMlWarps, kMlRegion, 0>;
@@ -1350,9 +1353,10 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
       xy = a.ml_state[j];
     }
   };
-  uint32_t np0, ny0, np1, ny1;
-  load(u + nw, np0, ny0);
-  load(u + 2 * nw, np1, ny1);
+  constexpr int PF = EG_ML_PF;  // units in flight ahead of the current one
+  uint32_t npf[PF], nyf[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) load(u + (k + 1) * nw, npf[k], nyf[k]);
   bool live = u < nu;  // warp-uniform
   uint32_t fill = 0;
   for (;;) {
@@ -1368,13 +1372,16 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
         }
         idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = np0;
-        pos = ok ? (ny0 & 0x1fffffffu) : B;
-        s = ny0 >> 29;
+        p = npf[0];
+        pos = ok ? (nyf[0] & 0x1fffffffu) : B;
+        s = nyf[0] >> 29;
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
-        np0 = np1;
-        ny0 = ny1;
-        load(u + 2 * nw, np1, ny1);
+#pragma unroll
+        for (int k = 0; k + 1 < PF; ++k) {
+          npf[k] = npf[k + 1];
+          nyf[k] = nyf[k + 1];
+        }
+        load(u + PF * nw, npf[PF - 1], nyf[PF - 1]);
         continue;
       }
       if (v) {
