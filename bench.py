@@ -163,10 +163,11 @@ def run_ours(args):
             dist.all_reduce(count, op=dist.ReduceOp.SUM)
         return st
 
+    st = None
     for _ in range(args.warmup):
         st = step()
     torch.cuda.synchronize()
-    launches_per_step = st.kernel_launches
+    launches_per_step = st.kernel_launches if st is not None else 0
     # ---- timed region: K steps, L2 flushed between steps (untimed) ----
     times = []
     with ClockSampler(local) as clk:
@@ -178,8 +179,9 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step()
+            st_t = step()
             e1.record(stream)
+            launches_per_step = launches_per_step or st_t.kernel_launches
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         torch.cuda.synchronize()
