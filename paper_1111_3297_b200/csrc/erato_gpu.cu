@@ -243,8 +243,6 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
                                 (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
-  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(eg::FusedSmem)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_ml, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::MlSmem)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_far, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,7 +439,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       const double eh = (double)P.S * (8.0 / 15.0) * sum_recip;
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
-      CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 4));
+      CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
       CUDA_TRY(c->hits.ensure(((uint64_t)P.W * hcap + eg::kScTrash) * 4));  // + trash of the split scatter
       CUDA_TRY(c->hitcnt.ensure((uint64_t)P.W * 4));
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
@@ -474,7 +472,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sa.i_ml_end = iWS;
       sa.i_end = nprimes;
       sa.x0 = 2 * P.g0 + 1;
-      sa.ml_state = c->ml.as<uint32_t>();
+      sa.ml = c->ml.as<uint2>();
       sa.far_buckets = c->buckets.as<uint64_t>();
       sa.far_bcount = c->bcount.as<uint32_t>();
       sa.ring = ring;
@@ -513,8 +511,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     eg::GenArgs ga{};
     eg::BinArgs ba{};
     if (have_large) {
-      ga.ml_p = c->primes.as<uint32_t>() + iS;
-      ga.ml_state = c->ml.as<uint32_t>();
+      ga.ml = c->ml.as<uint2>();
       ga.nml = (uint32_t)nml;
       ga.noct = (uint32_t)std::min<uint64_t>(idense - iS, nml);
       ga.bcap = bcap;
@@ -548,26 +545,16 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
-    // large-prime path: k_scatter_ml + k_scatter_far (default), the single
-    // fused walk+sort kernel (ERATO_GPU_SCATTER=fused, or when 32-bit list
-    // offsets do not fit), or k_gen + k_bin (=genbin, or > 256 bins)
+    // large-prime path: k_scatter_ml + k_scatter_far (default), or k_gen +
+    // k_bin (ERATO_GPU_SCATTER=genbin, or when a wave has more than 256 tiles
+    // or ring slots, or 32-bit list offsets do not fit)
     const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
-    const bool sortable = ring <= (uint32_t)eg::kFsBins && P.W <= (uint32_t)eg::kFsBins;
-    const bool genbin = (sc_env && std::strcmp(sc_env, "genbin") == 0) || !sortable;
-    bool fused = !genbin && sc_env && std::strcmp(sc_env, "fused") == 0;
-    // the split kernels index lists and buckets with 32-bit offsets
+    const bool sortable = ring <= (uint32_t)eg::kScBins && P.W <= (uint32_t)eg::kScBins;
     const bool idx32 = (uint64_t)P.W * hcap + eg::kScTrash < (1ull << 32) &&
                        (uint64_t)ring * bcap + eg::kScTrash < (1ull << 32);
-    const bool split = !genbin && !fused && idx32;
-    if (!genbin && !split) fused = true;
-    eg::FusedArgs fa{};
-    uint32_t fused_blocks = c->nsm, ml_blocks = c->nsm, far_blocks = c->nsm;
-    if (fused) {
-      int occ = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_fused, eg::kFsThreads,
-                                                             sizeof(eg::FusedSmem)));
-      fused_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
-    }
+    const bool split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
+    eg::ScatterArgs sca{};
+    uint32_t ml_blocks = c->nsm, far_blocks = c->nsm;
     if (split) {
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml, eg::kMlWarps * 32,
@@ -578,22 +565,20 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       far_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
     }
     if (have_large) {
-      fa.ml_p = ga.ml_p;
-      fa.ml_state = ga.ml_state;
-      fa.nml = ga.nml;
-      fa.noct = ga.noct;
-      fa.far_buckets = c->buckets.as<uint64_t>();
-      fa.far_bcount = c->bcount.as<uint32_t>();
-      fa.bcap = bcap;
-      fa.ring = ring;
-      fa.nwaves = P.nwaves;
-      fa.WS = P.WS;
-      fa.log_s = P.log_s;
-      fa.inv_ws = 1.0 / (double)P.WS;
-      fa.hits = c->hits.as<uint32_t>();
-      fa.hitcnt = c->hitcnt.as<uint32_t>();
-      fa.hcap = hcap;
-      fa.overflow = ga.overflow;
+      sca.ml = ga.ml;
+      sca.nml = ga.nml;
+      sca.far_buckets = c->buckets.as<uint64_t>();
+      sca.far_bcount = c->bcount.as<uint32_t>();
+      sca.bcap = bcap;
+      sca.ring = ring;
+      sca.nwaves = P.nwaves;
+      sca.WS = P.WS;
+      sca.log_s = P.log_s;
+      sca.inv_ws_f = 1.0f / (float)P.WS;
+      sca.hits = c->hits.as<uint32_t>();
+      sca.hitcnt = c->hitcnt.as<uint32_t>();
+      sca.hcap = hcap;
+      sca.overflow = ga.overflow;
     }
     const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
     const size_t nev = timing ? (size_t)P.nwaves * 5 + 8 : 0;
@@ -616,31 +601,20 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
         if (split) {
-          fa.wave = w;
-          fa.ntiles_w = ntw;
-          fa.far_in = ga.far_in;
-          fa.far_in_count = ga.far_in_count;
+          sca.wave = w;
+          sca.wslot = slot;
+          sca.ntiles_w = ntw;
+          sca.far_in = ga.far_in;
+          sca.far_in_count = ga.far_in_count;
           if (nml) {
-            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(fa);
+            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(sca);
             launches += 1;
           }
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           if (nfar) {
-            eg::FarArgs far{};
-            far.f = fa;
-            far.wslot = slot;
-            far.inv_ws_f = 1.0f / (float)P.WS;
-            eg::k_scatter_far<<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(far);
+            eg::k_scatter_far<<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
             launches += 1;
           }
-        } else if (fused) {
-          fa.wave = w;
-          fa.ntiles_w = ntw;
-          fa.far_in = ga.far_in;
-          fa.far_in_count = ga.far_in_count;
-          eg::k_scatter_fused<<<fused_blocks, eg::kFsThreads, sizeof(eg::FusedSmem), st>>>(fa);
-          if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
-          launches += 1;
         } else {
           eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));

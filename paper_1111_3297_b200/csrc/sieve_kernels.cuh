@@ -449,8 +449,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 // ML primes with p <= WS/8 are walked by 8 lanes (lane j of an octet: wheel
 // class (s+j)&7, step 15p), the others one per lane.
 struct GenArgs {
-  const uint32_t* ml_p;  // ML primes, ascending
-  uint32_t* ml_state;    // pos | s << 29
+  uint2* ml;             // ML primes, ascending: {p, pos | s << 29}
   uint32_t nml, noct;    // the first noct ML primes are walked by octets
   const uint64_t* far_in;  // far bucket of this wave
   const uint32_t* far_in_count;
@@ -510,8 +509,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     uint64_t u = gw;
     uint32_t pn = 0, stn = 0;
     if (u < uo && u * 4 + (lane >> 3) < a.noct) {
-      pn = a.ml_p[u * 4 + (lane >> 3)];
-      stn = a.ml_state[u * 4 + (lane >> 3)];
+      const uint2 e = a.ml[u * 4 + (lane >> 3)];
+      pn = e.x;
+      stn = e.y;
     }
     for (; u < uo; u += nw) {
       const uint64_t i = u * 4 + (lane >> 3);
@@ -519,8 +519,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
       const uint32_t p = pn, st = stn;
       const uint64_t inx = (u + nw) * 4 + (lane >> 3);
       if (u + nw < uo && inx < a.noct) {
-        pn = a.ml_p[inx];
-        stn = a.ml_state[inx];
+        const uint2 e = a.ml[inx];
+        pn = e.x;
+        stn = e.y;
       }
       const uint32_t s0 = st >> 29;
       uint32_t pos = ok ? (st & 0x1fffffffu) + p * nib(s_cum[s0], j) : WS;
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
       m = min(m, __shfl_xor_sync(kFull, m, 2));
       m = min(m, __shfl_xor_sync(kFull, m, 4));
       const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
-      if (ok && j == 0) a.ml_state[i] = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
+      if (ok && j == 0) a.ml[i].y = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
     }
   }
   // single ML primes: one per lane (next step's data prefetched)
@@ -546,8 +547,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     uint64_t u = gw;
     uint32_t pn = 0, stn = 0;
     if (u < us && a.noct + u * 32 + lane < a.nml) {
-      pn = a.ml_p[a.noct + u * 32 + lane];
-      stn = a.ml_state[a.noct + u * 32 + lane];
+      const uint2 e = a.ml[a.noct + u * 32 + lane];
+      pn = e.x;
+      stn = e.y;
     }
     for (; u < us; u += nw) {
       const uint64_t i = a.noct + u * 32 + lane;
@@ -555,8 +557,9 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
       const uint32_t p = pn, st = stn;
       const uint64_t inx = a.noct + (u + nw) * 32 + lane;
       if (u + nw < us && inx < a.nml) {
-        pn = a.ml_p[inx];
-        stn = a.ml_state[inx];
+        const uint2 e = a.ml[inx];
+        pn = e.x;
+        stn = e.y;
       }
       uint32_t pos = ok ? (st & 0x1fffffffu) : WS;
       uint32_t s = st >> 29;
@@ -568,7 +571,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
           s = (s + 1) & 7;
         }
       }
-      if (ok) a.ml_state[i] = (pos - WS) | (s << 29);
+      if (ok) a.ml[i].y = (pos - WS) | (s << 29);
     }
   }
   // far: exactly one hit in this wave, then re-bucket
@@ -881,454 +884,194 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_scatter_fused: the large-prime path of one wave in ONE kernel.
-// Each warp walks its share of the large primes — octets of 8 lanes per ML
-// prime with p <= WS/8 (lane j: wheel class (s+j)&7, step 15p), one lane per
-// ML prime above, one lane per entry of the wave's far bucket — and appends
-// one record (its position in the wave) per wheel-admissible multiple to its
-// private shared-memory region (ballot/popc compaction, no atomics).  When
-// the next step could overflow a region the warp pauses (its walk state
-// stays in registers) and the CTA runs a round: counting sort of all staged
-// records by tile, one global atomicAdd per (round, tile) reserving a run,
-// coalesced flushes into the per-tile hit lists.  Far entries re-bucketed
-// into the wave of their next hit (Lemma 2) are staged and
-// flushed the same way by ring slot.  Records never reach HBM unsorted.
-struct FusedArgs {
-  const uint32_t* ml_p;  // ML primes, ascending
-  uint32_t* ml_state;    // pos | s << 29
-  uint32_t nml, noct;    // the first noct ML primes are walked by octets
-  const uint64_t* far_in;  // far bucket of this wave
+// Large-prime scatter (default path), two kernels per wave:
+//  k_scatter_ml   walks the ML primes (S < p <= WS), one lane per prime,
+//                 resumable per step: a warp walks until its staging area is
+//                 full, not until its primes are done;
+//  k_scatter_far  takes the wave's far bucket (p > WS): exactly one hit in
+//                 the wave, then the entry moves to the bucket of the wave of
+//                 its next hit, k or k+1 waves ahead (Lemma 2,
+//                 the paper's in-place bucket sort,
+//                 large_kernel.hpp:61-213, as a ring of per-wave buckets).
+// Every hit becomes one u32 record (its position in the wave).  A warp stages
+// one record per lane per step in shared memory at [step][lane] (no ballot
+// compaction: an idle lane stores a sentinel), with its rank among this
+// round's records of the same tile — the value of the shared tile counter
+// the lane bumps when it emits.  When a warp's area is full the CTA runs a
+// round: a scan of the tile counts and one global atomicAdd per non-empty
+// tile reserving a run in that tile's hit list; records are placed in tile
+// order at off[tile] + rank (no atomics) and written as coalesced runs.
+// Re-bucketed far entries (8 B) go from staging straight to
+// bucket[reserved + rank].
+struct ScatterArgs {
+  uint2* ml;  // ML primes, ascending: {p, pos | s << 29} (pos = next hit from the current wave start)
+  uint32_t nml;
+  const uint64_t* far_in;  // far bucket of this wave: p | (q | s << 29) << 32
   const uint32_t* far_in_count;
-  uint64_t* far_buckets;  // [ring][bcap]
+  uint64_t* far_buckets;  // [ring][bcap] + trash
   uint32_t* far_bcount;
-  uint32_t bcap, ring;
+  uint32_t bcap, ring, wslot;  // wslot = wave % ring
   uint64_t wave, nwaves;
   uint32_t WS, ntiles_w, log_s;
-  double inv_ws;
-  uint32_t* hits;    // [ntiles_w][hcap]
+  float inv_ws_f;  // 1 / WS
+  uint32_t* hits;    // [ntiles_w][hcap] + trash
   uint32_t* hitcnt;  // [ntiles_w]
   uint32_t hcap;
   int* overflow;
 };
 
-#ifndef EG_FS_THREADS
-#define EG_FS_THREADS 256  // measured best on B200 with 640-record regions (4 CTAs/SM)
-#endif
-#ifndef EG_FS_REGION
-#define EG_FS_REGION 640
-#endif
-constexpr int kFsThreads = EG_FS_THREADS;
-constexpr int kFsWarps = kFsThreads / 32;
-static_assert(kFsThreads >= 128, "fs_flush needs two scanning warps plus reservation threads");
-constexpr int kFsRegion = EG_FS_REGION;  // staged records per warp
-#ifndef EG_FS_FAR
-#define EG_FS_FAR 64  // larger far staging costs occupancy (measured slower)
-#endif
-constexpr int kFsFar = EG_FS_FAR;  // staged re-bucketed far entries per warp
-constexpr int kFsBins = 256;    // >= tiles per wave and >= ring slots
+constexpr int kScBins = 256;            // >= tiles per wave and >= ring slots
+constexpr uint32_t kNoRec = 0xffffffffu;  // staged-slot sentinel (idle lane)
+constexpr uint8_t kNoSlot = 0xff;
 
-struct FusedSmem {
-  uint32_t reg[kFsWarps * kFsRegion];  // staged records, warp w at [w * kFsRegion]
-  uint32_t srt[kFsWarps * kFsRegion];  // sorted by tile
-  uint64_t freg[kFsWarps * kFsFar];
-  uint64_t fsrt[kFsWarps * kFsFar];
-  uint8_t fslot[kFsWarps * kFsFar];
-  uint8_t fsrt_slot[kFsWarps * kFsFar];
-  uint32_t fill[kFsWarps], ffill[kFsWarps];
-  uint32_t cnt[kFsBins], off[kFsBins], base[kFsBins];
-  uint32_t fcnt[kFsBins], foff[kFsBins], fbase[kFsBins];
-  uint32_t cum[8];
-  uint32_t total, ftotal;
-};
-
-// sort the staged records of all warps by tile (far entries by slot), flush
-__device__ void fs_flush(FusedSmem& sm, const FusedArgs& a) {
-  const uint32_t tid = threadIdx.x, nb = a.ntiles_w, shift = a.log_s, ring = a.ring;
-  constexpr uint32_t R = kFsRegion, F = kFsFar;
-  // count: each warp walks its own region's filled slots
-  const uint32_t lane = tid & 31, warp = tid >> 5;
-  {
-    const uint32_t* rg = sm.reg + warp * R;
-    const uint32_t n = sm.fill[warp];
-    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&sm.cnt[rg[i] >> shift], 1u);
-    const uint8_t* fs = sm.fslot + warp * F;
-    const uint32_t fn = sm.ffill[warp];
-    for (uint32_t i = lane; i < fn; i += 32) atomicAdd(&sm.fcnt[fs[i]], 1u);
-  }
-  __syncthreads();
-  if (tid < 32) {
-    const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
-    if (tid == 0) sm.total = tot;
-  } else if (tid < 64) {
-    const uint32_t tot = warp_excl_scan(sm.fcnt, sm.foff, ring);
-    if (tid == 32) sm.ftotal = tot;
-  }
-  // global reservations: one atomicAdd per non-empty tile / ring slot,
-  // strided over the threads outside the two scanning warps
-  if (tid >= 64) {
-    for (uint32_t b = tid - 64; b < nb + ring; b += blockDim.x - 64) {
-      if (b < nb) {
-        const uint32_t c = sm.cnt[b];
-        if (c) {
-          const uint32_t r = atomicAdd(&a.hitcnt[b], c);
-          sm.base[b] = r;
-          if (r + c > a.hcap) atomicExch(a.overflow, 1);
-        }
-      } else {
-        const uint32_t t = b - nb, c = sm.fcnt[t];
-        if (c) {
-          const uint32_t r = atomicAdd(&a.far_bcount[t], c);
-          sm.fbase[t] = r;
-          if (r + c > a.bcap) atomicExch(a.overflow, 1);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
-  for (uint32_t t = tid; t < ring; t += blockDim.x) sm.fcnt[t] = 0;
-  __syncthreads();
-  // place
-  {
-    const uint32_t* rg = sm.reg + warp * R;
-    const uint32_t n = sm.fill[warp];
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t key = rg[i];
-      const uint32_t t = key >> shift;
-      sm.srt[sm.off[t] + atomicAdd(&sm.cnt[t], 1u)] = key;
-    }
-    const uint32_t fn = sm.ffill[warp];
-    for (uint32_t i = lane; i < fn; i += 32) {
-      const uint32_t t = sm.fslot[warp * F + i];
-      const uint32_t k = sm.foff[t] + atomicAdd(&sm.fcnt[t], 1u);
-      sm.fsrt[k] = sm.freg[warp * F + i];
-      sm.fsrt_slot[k] = (uint8_t)t;
-    }
-  }
-  __syncthreads();
-  // flush: consecutive sorted slots of one tile -> consecutive addresses
-  const uint32_t total = sm.total, smask = (1u << shift) - 1;
-  for (uint32_t i = tid; i < total; i += blockDim.x) {
-    const uint32_t key = sm.srt[i];
-    const uint32_t t = key >> shift;
-    EG_CHECK(t < nb && i >= sm.off[t], "fs flush t=%u nb=%u i=%u off=%u", t, nb, i, sm.off[t]);
-    const uint32_t slot = sm.base[t] + (i - sm.off[t]);
-    if (slot < a.hcap) a.hits[(uint64_t)t * a.hcap + slot] = key & smask;
-  }
-  const uint32_t ft = sm.ftotal;
-  for (uint32_t i = tid; i < ft; i += blockDim.x) {
-    const uint32_t t = sm.fsrt_slot[i];
-    const uint32_t pos = sm.fbase[t] + (i - sm.foff[t]);
-    if (pos < a.bcap) a.far_buckets[(uint64_t)t * a.bcap + pos] = sm.fsrt[i];
-  }
-  __syncthreads();
-  for (uint32_t t = tid; t < nb; t += blockDim.x) sm.cnt[t] = 0;
-  for (uint32_t t = tid; t < ring; t += blockDim.x) sm.fcnt[t] = 0;
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(kFsThreads) k_scatter_fused(const FusedArgs a) {
-  extern __shared__ uint4 smem_raw[];
-  FusedSmem& sm = *reinterpret_cast<FusedSmem*>(smem_raw);
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt = (1u << lane) - 1;
-  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) {
-    sm.cnt[t] = 0;
-    sm.fcnt[t] = 0;
-  }
-  if (tid < 8) {
-    uint32_t v = 0;
-    for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
-    sm.cum[tid] = v;
-  }
-  __syncthreads();
-  const uint32_t WS = a.WS;
-  const uint32_t lim = a.ntiles_w << a.log_s;  // positions past the wave's last tile are dropped
-  const uint64_t gw = (uint64_t)blockIdx.x * kFsWarps + warp;
-  const uint64_t nw = (uint64_t)gridDim.x * kFsWarps;
-  const uint32_t nfar = a.far_in ? min(*a.far_in_count, a.bcap) : 0;
-  const uint64_t uo = (a.noct + 3) / 4, us = (a.nml - a.noct + 31) / 32, uf = (nfar + 31) / 32;
-  uint32_t* const myreg = sm.reg + warp * kFsRegion;
-  uint64_t* const myfreg = sm.freg + warp * kFsFar;
-  uint8_t* const myfslot = sm.fslot + warp * kFsFar;
-  uint32_t fill = 0, ffill = 0;  // warp-uniform
-
-  // Units are walked whole; a warp pauses between units once its region
-  // could not take a worst-case unit (octet: 4 primes x 80 admissible hits
-  // per wave for W <= 150; single: 32 x 8; far: 32 records + 32 entries).
-  constexpr uint32_t kUnitMax = 320;
-  int phase = 0;  // 0 octets, 1 singles, 2 far, 3 done
-  uint64_t u = gw;
-  auto units_of = [&](int ph) { return ph == 0 ? uo : ph == 1 ? us : uf; };
-  while (phase < 3 && u >= units_of(phase)) {
-    ++phase;
-    u = gw;
-  }
-  // prefetched raw data of the next unit
-  auto fetch = [&](int ph, uint64_t uu, uint32_t& x, uint32_t& y) {
-    x = 0;
-    y = 0;
-    if (ph == 0) {
-      const uint64_t ix = uu * 4 + (lane >> 3);
-      if (ix < a.noct) {
-        x = a.ml_p[ix];
-        y = a.ml_state[ix];
-      }
-    } else if (ph == 1) {
-      const uint64_t ix = a.noct + uu * 32 + lane;
-      if (ix < a.nml) {
-        x = a.ml_p[ix];
-        y = a.ml_state[ix];
-      }
-    } else if (ph == 2) {
-      const uint64_t ix = uu * 32 + lane;
-      if (ix < nfar) {
-        const uint64_t e = a.far_in[ix];
-        x = (uint32_t)e;
-        y = (uint32_t)(e >> 32);
-      }
-    }
-  };
-  uint32_t nx = 0, ny = 0;
-  if (phase < 3) fetch(phase, u, nx, ny);
-
-  for (;;) {
-    while (phase < 3 && fill + kUnitMax <= (uint32_t)kFsRegion && ffill + 32 <= (uint32_t)kFsFar) {
-      const int ph = phase;
-      const uint64_t cu = u;
-      const uint32_t x = nx, y = ny;
-      // advance to the next unit and prefetch it
-      u += nw;
-      while (phase < 3 && u >= units_of(phase)) {
-        ++phase;
-        u = gw;
-      }
-      if (phase < 3) fetch(phase, u, nx, ny);
-      if (ph == 0) {
-        const uint64_t idx = cu * 4 + (lane >> 3);
-        const bool ok = idx < a.noct;
-        const uint32_t p = x, s0 = y >> 29;
-        uint32_t pos = ok ? (y & 0x1fffffffu) + p * nib(sm.cum[s0], lane & 7) : WS;
-        const uint32_t step = 15u * p;
-        while (__any_sync(kFull, pos < WS)) {
-          const bool v = pos < WS;
-          const bool emit = v && pos < lim;
-          const uint32_t m = __ballot_sync(kFull, emit);
-          if (emit) myreg[fill + __popc(m & lt)] = pos;
-          fill += __popc(m);
-          if (v) pos += step;
-        }
-        const uint32_t ex = pos - WS;
-        uint32_t mn = ex;
-        mn = min(mn, __shfl_xor_sync(kFull, mn, 1));
-        mn = min(mn, __shfl_xor_sync(kFull, mn, 2));
-        mn = min(mn, __shfl_xor_sync(kFull, mn, 4));
-        const uint32_t bal = (__ballot_sync(kFull, ex == mn) >> (lane & ~7u)) & 0xffu;
-        if (ok && (lane & 7) == 0) a.ml_state[idx] = mn | (((s0 + __ffs(bal) - 1) & 7) << 29);
-      } else if (ph == 1) {
-        const uint64_t idx = a.noct + cu * 32 + lane;
-        const bool ok = idx < a.nml;
-        const uint32_t p = x;
-        uint32_t pos = ok ? (y & 0x1fffffffu) : WS, s = y >> 29;
-        while (__any_sync(kFull, pos < WS)) {
-          const bool v = pos < WS;
-          const bool emit = v && pos < lim;
-          const uint32_t m = __ballot_sync(kFull, emit);
-          if (emit) myreg[fill + __popc(m & lt)] = pos;
-          fill += __popc(m);
-          if (v) {
-            pos += wheel_D(s) * p;
-            s = (s + 1) & 7;
-          }
-        }
-        if (ok) a.ml_state[idx] = (pos - WS) | (s << 29);
-      } else {
-        const uint64_t idx = cu * 32 + lane;
-        const bool ok = idx < nfar;
-        const uint32_t p = x, q = y & 0x1fffffffu, s = y >> 29;
-        const bool emit = ok && q < lim;
-        const uint32_t m = __ballot_sync(kFull, emit);
-        if (emit) myreg[fill + __popc(m & lt)] = q;
-        fill += __popc(m);
-        // the entry moves to the wave of its next hit (Lemma 2)
-        bool keep = false;
-        uint64_t ne = 0;
-        uint32_t slot = 0;
-        if (ok) {
-          const uint64_t q2 = (uint64_t)q + (uint64_t)wheel_D(s) * p;
-          uint64_t d = (uint64_t)((double)q2 * a.inv_ws);
-          while (d * WS > q2) --d;
-          while ((d + 1) * WS <= q2) ++d;
-          const uint64_t tgt = a.wave + d;
-          if (tgt < a.nwaves) {
-            keep = true;
-            slot = (uint32_t)tgt % a.ring;
-            ne = (uint64_t)p | ((uint64_t)((uint32_t)(q2 - d * WS) | (((s + 1) & 7) << 29)) << 32);
-          }
-        }
-        const uint32_t fm = __ballot_sync(kFull, keep);
-        if (keep) {
-          const uint32_t k = ffill + __popc(fm & lt);
-          myfreg[k] = ne;
-          myfslot[k] = (uint8_t)slot;
-        }
-        ffill += __popc(fm);
-      }
-    }
-    if (lane == 0) {
-      sm.fill[warp] = fill;
-      sm.ffill[warp] = ffill;
-    }
-    const int more = __syncthreads_or(phase < 3);
-    fs_flush(sm, a);
-    fill = 0;
-    ffill = 0;
-    if (!more) break;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Split large-prime path: k_scatter_ml walks the ML primes (S < p <= WS),
-// k_scatter_far the far bucket of the wave.  Same staging/sort/flush scheme as
-// k_scatter_fused, but each kernel has one kind of unit, so
-//  * the ML walk is resumable per step (one lane per prime, all ML primes):
-//    a warp walks until its region is full, not until a unit ends, and every
-//    round flushes nearly full regions;
-//  * the far kernel sizes its staging for far entries (one per lane per
-//    unit), so far rounds are ~8x rarer than with 64-entry staging;
-//  * no phase machine, and the far next-wave index is an fp32 estimate plus
-//    an exact 32-bit wrap-around correction instead of fp64 + u64 division.
-template <int NW, int R, int F>
+template <int NW, int SL, bool FAR>
 struct ScSmem {
-  static constexpr int FF = F > 0 ? F : 1;
-  uint32_t reg[NW * R];  // staged records, warp w at [w * R]
-  uint32_t srt[NW * R];  // sorted by tile
-  uint64_t freg[NW * FF];
-  uint16_t frank[NW * FF];  // rank among this round's entries of the same slot
-  uint8_t fslot[NW * FF];
-  uint32_t fill[NW], ffill[NW];
-  // cnt: per-round counts (bumped at emission), then placement cursors;
-  // gofs[t] = global index of sorted slot 0 of bin t (t*cap + reserved - off)
-  uint32_t cnt[kFsBins], off[kFsBins], gofs[kFsBins];
-  uint32_t fcnt[kFsBins], fgofs[kFsBins];
+  static constexpr int R = SL * 32;  // staged records per warp
+  static constexpr int RS = R + 32;  // + per-lane trash slots (compacting ML emission)
+  static constexpr int FR = FAR ? R : 1;
+  uint32_t reg[NW * RS];   // warp w, step k, lane j at [w*RS + k*32 + j]
+  uint16_t rank[NW * RS];  // rank among this round's records of the same tile
+  uint32_t srt[NW * R];   // this round's records sorted by tile
+  uint64_t freg[NW * FR];
+  uint16_t frank[NW * FR];
+  uint8_t fslot[NW * FR];
+  // cnt: per-round counts (bumped at emission; [kScBins + lane] = sinks of
+  // idle lanes, one per lane: no same-address conflicts); off: their
+  // exclusive scan; gofs[t] = global index of sorted slot 0 of tile t
+  // (t*cap + reserved - off)
+  uint32_t cnt[kScBins + 32], off[kScBins], gofs[kScBins];
+  uint32_t fcnt[kScBins + 32], fgofs[kScBins];
   uint32_t total;
-  static_assert(NW * FF < 65536, "far ranks are 16-bit");
+  static_assert(NW * R < 65536, "ranks are 16-bit");
 };
 
-// Round of the split scatter kernels: the staged records of every warp were
-// already counted per tile (far entries per ring slot) while they were
-// emitted.  Scan, one global reservation per non-empty bin, placement into
-// tile order, coalesced flush.  A bin whose reservation overflows its list
-// is redirected to the trash area past the lists (the host retries the run
-// with larger lists when the overflow flag is set).
-template <int NW, int R, int F>
-__device__ void sc_flush(ScSmem<NW, R, F>& sm, const FusedArgs& a) {
+// Shared-memory helpers for the emission loops: 32-bit shared addresses kept
+// in registers (volatile: computed once, not rematerialised in the loop).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  uint32_t r;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+  return r;
+}
+// r = atomicAdd(cnt, 1) and the record store (unconditional: idle lanes
+// count into their sink and stage the sentinel).  The rank r is stored one
+// step later (st_rank), so the atomic's latency overlaps the next step.
+__device__ __forceinline__ uint32_t stage_rec(uint32_t cnt_addr, uint32_t reg_addr, uint32_t val) {
+  uint32_t r;
+  asm volatile(
+      "atom.shared.add.u32 %0, [%1], 1;\n\t"
+      "st.shared.u32 [%2], %3;"
+      : "=r"(r)
+      : "r"(cnt_addr), "r"(reg_addr), "r"(val)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ uint32_t stage_far(uint32_t cnt_addr, uint32_t ent_addr, uint32_t slot_addr, uint64_t ent,
+                                              uint32_t slot) {
+  uint32_t r;
+  asm volatile(
+      "atom.shared.add.u32 %0, [%1], 1;\n\t"
+      "st.shared.u64 [%2], %4;\n\t"
+      "st.shared.u8 [%3], %5;"
+      : "=r"(r)
+      : "r"(cnt_addr), "r"(ent_addr), "r"(slot_addr), "l"(ent), "r"(slot)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_rank(uint32_t addr, uint32_t r) {
+  asm volatile("st.shared.u16 [%0], %1;" : : "r"(addr), "r"(r) : "memory");
+}
+
+template <int NW, int SL, bool FAR>
+__device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterArgs& a, uint32_t n) {
+  using Sm = ScSmem<NW, SL, FAR>;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nb = a.ntiles_w, shift = a.log_s, ring = F > 0 ? a.ring : 0;
-  constexpr uint32_t NT = NW * 32, FF = ScSmem<NW, R, F>::FF;
-  constexpr uint32_t kScan = 32;  // scanning threads
-  // (the caller's barrier orders the emission-time counts before the scan)
+  constexpr uint32_t NT = NW * 32;
+  const uint32_t nb = a.ntiles_w, ring = FAR ? a.ring : 0;
   if (tid < 32) {
     const uint32_t tot = warp_excl_scan(sm.cnt, sm.off, nb);
     if (tid == 0) sm.total = tot;
   } else {
-    for (uint32_t b = tid - kScan; b < nb + ring; b += NT - kScan) {
+    for (uint32_t b = tid - 32; b < nb + ring; b += NT - 32) {
       if (b < nb) {
         const uint32_t c = sm.cnt[b];
         if (c) {
           const uint32_t r = atomicAdd(&a.hitcnt[b], c);
           const bool over = r + c > a.hcap;
           if (over) atomicExch(a.overflow, 1);
-          sm.gofs[b] = over ? 0xffffffffu : b * a.hcap + r;
+          sm.gofs[b] = over ? nb * a.hcap : b * a.hcap + r;
         }
-      } else {
+      } else if constexpr (FAR) {
         const uint32_t t = b - nb, c = sm.fcnt[t];
         if (c) {
+          sm.fcnt[t] = 0;  // nobody counts again before the next barrier
           const uint32_t r = atomicAdd(&a.far_bcount[t], c);
           const bool over = r + c > a.bcap;
           if (over) atomicExch(a.overflow, 1);
-          sm.fgofs[t] = over ? 0xffffffffu : t * a.bcap + r;
+          sm.fgofs[t] = over ? a.ring * a.bcap : t * a.bcap + r;
         }
       }
     }
   }
   __syncthreads();
-  // cursors and final offsets
-  const uint32_t trash = nb * a.hcap;  // the hit lists of this wave end here
-  for (uint32_t t = tid; t < nb; t += NT) {
-    const uint32_t o = sm.off[t];
-    const uint32_t g = sm.gofs[t];
-    if (sm.cnt[t]) sm.gofs[t] = (g == 0xffffffffu ? trash : g) - o;
-    sm.cnt[t] = o;
-  }
-  if constexpr (F > 0) {
-    // far entries go straight from staging to their bucket run: the
-    // emission-time count returned each entry's rank within (round, slot)
-    const uint32_t ftrash = a.ring * a.bcap;
-    for (uint32_t t = tid; t < ring; t += NT)
-      if (sm.fcnt[t] && sm.fgofs[t] == 0xffffffffu) sm.fgofs[t] = ftrash;
-  }
-  __syncthreads();
+  const uint32_t shift = a.log_s, smask = (1u << shift) - 1;
   {
-    const uint32_t* rg = sm.reg + warp * R;
-    const uint32_t n = sm.fill[warp];
+    const uint32_t* rg = sm.reg + warp * Sm::RS;
+    const uint16_t* rk = sm.rank + warp * Sm::RS;
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = rg[i];
-      sm.srt[atomicAdd(&sm.cnt[key >> shift], 1u)] = key;
-    }
-    if constexpr (F > 0) {
-      const uint32_t fn = sm.ffill[warp];
-      for (uint32_t i = lane; i < fn; i += 32) {
-        const uint32_t j = warp * FF + i;
-        a.far_buckets[sm.fgofs[sm.fslot[j]] + sm.frank[j]] = sm.freg[j];
-      }
+      if (key != kNoRec) sm.srt[sm.off[key >> shift] + rk[i]] = key;
     }
   }
+  if constexpr (FAR) {
+    const uint32_t base = warp * Sm::FR;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t t = sm.fslot[base + i];
+      if (t != kNoSlot) a.far_buckets[sm.fgofs[t] + sm.frank[base + i]] = sm.freg[base + i];
+    }
+  }
+  for (uint32_t b = tid; b < nb; b += NT) {
+    if (sm.cnt[b]) sm.gofs[b] -= sm.off[b];
+    sm.cnt[b] = 0;
+  }  // (the sinks are never read: their counts may wrap)
   __syncthreads();
-  const uint32_t total = sm.total, smask = (1u << shift) - 1;
+  const uint32_t total = sm.total;
   for (uint32_t i = tid; i < total; i += NT) {
     const uint32_t key = sm.srt[i];
     a.hits[sm.gofs[key >> shift] + i] = key & smask;
   }
-  __syncthreads();
-  for (uint32_t t = tid; t < nb; t += NT) sm.cnt[t] = 0;
-  if constexpr (F > 0)
-    for (uint32_t t = tid; t < ring; t += NT) sm.fcnt[t] = 0;
-  __syncthreads();  // counts are zero before any warp emits again
+  // off/gofs/srt are rewritten only after the next round's first barrier
 }
 
 #ifndef EG_ML_WARPS
 #define EG_ML_WARPS 8
 #endif
-#ifndef EG_ML_REGION
-#define EG_ML_REGION 384
+#ifndef EG_ML_STEPS
+#define EG_ML_STEPS 12
+#endif
+#ifndef EG_ML_COMPACT
+#define EG_ML_COMPACT 0
 #endif
 #ifndef EG_FAR_WARPS
 #define EG_FAR_WARPS 8
 #endif
-#ifndef EG_FAR_REGION
-#define EG_FAR_REGION 192
+#ifndef EG_FAR_STEPS
+#define EG_FAR_STEPS 6
 #endif
-#ifndef EG_ML_PF
-#define EG_ML_PF 1
-#endif
-constexpr int kMlWarps = EG_ML_WARPS, kMlRegion = EG_ML_REGION;
-constexpr int kFarWarps = EG_FAR_WARPS, kFarRegion = EG_FAR_REGION;
-using MlSmem = ScSmem<kMlWarps, kMlRegion, 0>;
-using FarSmem = ScSmem<kFarWarps, kFarRegion, kFarRegion>;
-// records one round may send to the trash area (per CTA)
-constexpr uint32_t kScTrash = (uint32_t)(kMlWarps * kMlRegion > kFarWarps * kFarRegion ? kMlWarps * kMlRegion
-                                                                                        : kFarWarps * kFarRegion);
-static_assert(kMlWarps >= 2 && kFarWarps >= 3, "sc_flush needs scanning warps plus reservation threads");
+constexpr int kMlWarps = EG_ML_WARPS, kMlSteps = EG_ML_STEPS;
+constexpr int kFarWarps = EG_FAR_WARPS, kFarSteps = EG_FAR_STEPS;
+using MlSmem = ScSmem<kMlWarps, kMlSteps, false>;
+using FarSmem = ScSmem<kFarWarps, kFarSteps, true>;
+// records / entries one round may send to the trash area
+constexpr uint32_t kScTrash = (uint32_t)(MlSmem::R * kMlWarps > FarSmem::R * kFarWarps ? MlSmem::R * kMlWarps
+                                                                                       : FarSmem::R * kFarWarps);
 
 __device__ __forceinline__ uint32_t rotr4(uint32_t x) { return __funnelshift_r(x, x, 4); }
 
-__global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a) {
+__global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs a) {
   extern __shared__ uint4 smem_raw[];
   MlSmem& sm = *reinterpret_cast<MlSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt = (1u << lane) - 1;
-  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) sm.cnt[t] = 0;
+  for (uint32_t t = tid; t < kScBins; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
   const uint32_t WS = a.WS, shift = a.log_s;
   // walk bound: the wave end, or the end of the last tile in the last wave
@@ -1336,35 +1079,49 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
   const uint32_t B = a.ntiles_w << a.log_s;
   const uint32_t nw = gridDim.x * kMlWarps;
   const uint32_t nu = (a.nml + 31) / 32;
-  uint32_t* const myreg = sm.reg + warp * kMlRegion;
+#if EG_ML_COMPACT
+  const uint32_t lt = (1u << lane) - 1;
+  const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::RS), rank_a = smem_addr(sm.rank + warp * MlSmem::RS);
+  const uint32_t treg_a = reg_a + 4 * (MlSmem::R + lane), trank_a = rank_a + 2 * (MlSmem::R + lane);
+#else
+  const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::RS + lane);
+  const uint32_t rank_a = smem_addr(sm.rank + warp * MlSmem::RS + lane);
+#endif
+  const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
   uint32_t u = blockIdx.x * kMlWarps + warp;
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nml;
-  uint32_t p = ok ? a.ml_p[idx] : 0, y = ok ? a.ml_state[idx] : 0;
+  uint2 e0 = ok ? a.ml[idx] : make_uint2(0, 0);
+  uint32_t p = e0.x, y = e0.y;
   uint32_t pos = ok ? (y & 0x1fffffffu) : B, s = y >> 29;
   uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
-  // the next two units' primes and states are in flight
-  auto load = [&](uint32_t uu, uint32_t& xp, uint32_t& xy) {
-    const uint32_t j = uu * 32 + lane;
-    xp = 0;
-    xy = 0;
-    if (uu < nu && j < a.nml) {
-      xp = a.ml_p[j];
-      xy = a.ml_state[j];
+  // the next unit's primes and states are in flight
+  uint32_t np = 0, ny = 0;
+  {
+    const uint32_t j = (u + nw) * 32 + lane;
+    if (u + nw < nu && j < a.nml) {
+      const uint2 e = a.ml[j];
+      np = e.x;
+      ny = e.y;
     }
-  };
-  constexpr int PF = EG_ML_PF;  // units in flight ahead of the current one
-  uint32_t npf[PF], nyf[PF];
-#pragma unroll
-  for (int k = 0; k < PF; ++k) load(u + (k + 1) * nw, npf[k], nyf[k]);
+  }
   bool live = u < nu;  // warp-uniform
-  uint32_t fill = 0;
   for (;;) {
-    while (live && fill + 32 <= (uint32_t)kMlRegion) {
+    bool rk_pend = false;  // the last staged rank is stored one step late
+    uint32_t rk_addr = 0, rk_val = 0;
+#if EG_ML_COMPACT
+    uint32_t k = 0;  // staged records (warp-uniform), compacted with a ballot
+    while (live && k <= (uint32_t)(MlSmem::R - 32)) {
       const bool v = pos < B;
       const uint32_t m = __ballot_sync(kFull, v);
       if (m == 0) {
-        if (ok) a.ml_state[idx] = (pos - WS) | ((s & 7) << 29);
+#else
+    uint32_t k = 0;  // staged steps (warp-uniform)
+    while (live && k < (uint32_t)kMlSteps) {
+      const bool v = pos < B;
+      if (!__any_sync(kFull, v)) {
+#endif
+        if (ok) a.ml[idx].y = (pos - WS) | ((s & 7) << 29);
         u += nw;
         if (u >= nu) {
           live = false;
@@ -1372,48 +1129,57 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const FusedArgs a)
         }
         idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = npf[0];
-        pos = ok ? (nyf[0] & 0x1fffffffu) : B;
-        s = nyf[0] >> 29;
+        p = np;
+        pos = ok ? (ny & 0x1fffffffu) : B;
+        s = ny >> 29;
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
-#pragma unroll
-        for (int k = 0; k + 1 < PF; ++k) {
-          npf[k] = npf[k + 1];
-          nyf[k] = nyf[k + 1];
+        const uint32_t j = (u + nw) * 32 + lane;
+        np = 0;
+        ny = 0;
+        if (u + nw < nu && j < a.nml) {
+          const uint2 e = a.ml[j];
+          np = e.x;
+          ny = e.y;
         }
-        load(u + PF * nw, npf[PF - 1], nyf[PF - 1]);
         continue;
       }
+#if EG_ML_COMPACT
+      const uint32_t kk = k + __popc(m & lt);
+      const uint32_t r = stage_rec(v ? cnt_a + ((pos >> shift) << 2) : sink_a, v ? reg_a + (kk << 2) : treg_a, pos);
+      if (rk_pend) st_rank(rk_addr, rk_val);
+      rk_pend = true;
+      rk_addr = v ? rank_a + (kk << 1) : trank_a;
+      rk_val = r;
+      k += __popc(m);
+#else
+      const uint32_t r = stage_rec(v ? cnt_a + ((pos >> shift) << 2) : sink_a, reg_a + (k << 7), v ? pos : kNoRec);
+      if (rk_pend) st_rank(rk_addr, rk_val);
+      rk_pend = true;
+      rk_addr = rank_a + (k << 6);
+      rk_val = r;
+      ++k;
+#endif
       if (v) {
-        myreg[fill + __popc(m & lt)] = pos;
-        atomicAdd(&sm.cnt[pos >> shift], 1u);
         pos += (dd & 15u) * p;
         dd = rotr4(dd);
         ++s;
       }
-      fill += __popc(m);
     }
-    if (lane == 0) sm.fill[warp] = fill;
+    if (rk_pend) st_rank(rk_addr, rk_val);
+#if !EG_ML_COMPACT
+    k *= 32;
+#endif
     const int more = __syncthreads_or(live);
-    sc_flush(sm, a);
-    fill = 0;
+    sc_flush(sm, a, k);
     if (!more) break;
   }
 }
 
-struct FarArgs {
-  FusedArgs f;
-  uint32_t wslot;   // wave % ring
-  float inv_ws_f;   // 1 / WS
-};
-
-__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa) {
+__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArgs a) {
   extern __shared__ uint4 smem_raw[];
   FarSmem& sm = *reinterpret_cast<FarSmem*>(smem_raw);
-  const FusedArgs& a = fa.f;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt = (1u << lane) - 1;
-  for (uint32_t t = tid; t < kFsBins; t += blockDim.x) {
+  for (uint32_t t = tid; t < kScBins; t += blockDim.x) {
     sm.cnt[t] = 0;
     sm.fcnt[t] = 0;
   }
@@ -1424,10 +1190,12 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
   const uint32_t nw = gridDim.x * kFarWarps;
   const uint32_t nu = (nfar + 31) / 32;
   const uint64_t left = a.nwaves - a.wave;  // waves from this one to the end
-  uint32_t* const myreg = sm.reg + warp * kFarRegion;
-  uint64_t* const myfreg = sm.freg + warp * kFarRegion;
-  uint8_t* const myfslot = sm.fslot + warp * kFarRegion;
-  uint16_t* const myfrank = sm.frank + warp * kFarRegion;
+  const uint32_t wofs = warp * FarSmem::R + lane;
+  const uint32_t reg_a = smem_addr(sm.reg + warp * FarSmem::RS + lane), rank_a = smem_addr(sm.rank + warp * FarSmem::RS + lane);
+  const uint32_t ent_a = smem_addr(sm.freg + wofs), slot_a = smem_addr(sm.fslot + wofs),
+                 frank_a = smem_addr(sm.frank + wofs);
+  const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
+  const uint32_t fcnt_a = smem_addr(sm.fcnt), fsink_a = fcnt_a + 4 * (kScBins + lane);
   uint32_t u = blockIdx.x * kFarWarps + warp;
   // the entries of the next two units are in flight (loads issued early)
   auto load = [&](uint32_t uu) -> uint64_t {
@@ -1435,9 +1203,10 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
     return (uu < nu && j < nfar) ? a.far_in[j] : 0;
   };
   uint64_t ne0 = load(u), ne1 = load(u + nw);
-  uint32_t fill = 0, ffill = 0;
+  uint32_t rk1 = 0, rk2 = 0;  // ranks of the last step, stored one step late
   for (;;) {
-    while (u < nu && fill + 32 <= (uint32_t)kFarRegion && ffill + 32 <= (uint32_t)kFarRegion) {
+    uint32_t k = 0;  // staged steps (warp-uniform)
+    for (; u < nu && k < (uint32_t)kFarSteps; ++k) {
       const uint32_t i = u * 32 + lane;
       const bool ok = i < nfar;
       const uint64_t e = ne0;
@@ -1446,16 +1215,16 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
       u += nw;
       const uint32_t p = (uint32_t)e, q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
       const bool emit = ok && q < lim;
-      const uint32_t m = __ballot_sync(kFull, emit);
-      if (emit) {
-        myreg[fill + __popc(m & lt)] = q;
-        atomicAdd(&sm.cnt[q >> shift], 1u);
+      const uint32_t r1 = stage_rec(emit ? cnt_a + ((q >> shift) << 2) : sink_a, reg_a + (k << 7), emit ? q : kNoRec);
+      if (k) {  // ranks of the previous step
+        st_rank(rank_a + ((k - 1) << 6), rk1);
+        st_rank(frank_a + ((k - 1) << 6), rk2);
       }
-      fill += __popc(m);
+      rk1 = r1;
       // next hit q + D*p lies d waves ahead (Lemma 2): fp32 estimate of d,
       // then the exact remainder in 32-bit wrap-around arithmetic
       const uint32_t D = wheel_D(s);
-      uint32_t d = __float2uint_rz(__fmaf_rn((float)D, (float)p, (float)q) * fa.inv_ws_f);
+      uint32_t d = __float2uint_rz(__fmaf_rn((float)D, (float)p, (float)q) * a.inv_ws_f);
       int32_t r = (int32_t)(q + D * p - d * WS);
       while (r < 0) {
         r += (int32_t)WS;
@@ -1466,25 +1235,17 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const FarArgs fa
         ++d;
       }
       const bool keep = ok && d < left;
-      uint32_t slot = fa.wslot + d;
+      uint32_t slot = a.wslot + d;
       if (slot >= ring) slot -= ring;
-      const uint32_t fm = __ballot_sync(kFull, keep);
-      if (keep) {
-        const uint32_t k = ffill + __popc(fm & lt);
-        myfreg[k] = (uint64_t)p | ((uint64_t)((uint32_t)r | (((s + 1) & 7) << 29)) << 32);
-        myfslot[k] = (uint8_t)slot;
-        myfrank[k] = (uint16_t)atomicAdd(&sm.fcnt[slot], 1u);
-      }
-      ffill += __popc(fm);
+      rk2 = stage_far(keep ? fcnt_a + (slot << 2) : fsink_a, ent_a + (k << 8), slot_a + (k << 5),
+                      (uint64_t)p | ((uint64_t)((uint32_t)r | (((s + 1) & 7) << 29)) << 32), keep ? slot : kNoSlot);
     }
-    if (lane == 0) {
-      sm.fill[warp] = fill;
-      sm.ffill[warp] = ffill;
+    if (k) {
+      st_rank(rank_a + ((k - 1) << 6), rk1);
+      st_rank(frank_a + ((k - 1) << 6), rk2);
     }
     const int more = __syncthreads_or(u < nu);
-    sc_flush(sm, a);
-    fill = 0;
-    ffill = 0;
+    sc_flush(sm, a, k * 32);
     if (!more) break;
   }
 }
@@ -1633,7 +1394,7 @@ struct SetupArgs {
   const uint32_t* primes;
   uint64_t i0, i_ml_end, i_end;  // ML = [i0, i_ml_end), far = [i_ml_end, i_end)
   uint64_t x0;                   // 2*g0 + 1
-  uint32_t* ml_state;
+  uint2* ml;
   uint64_t* far_buckets;
   uint32_t* far_bcount;
   uint32_t ring, bcap;
@@ -1655,7 +1416,7 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
     // keeps the first hit within 3.5p of the interval start in overlap runs
     const uint64_t pos = first_hit(p, ~0ull / p, a.x0, 2, s);
     if (i < a.i_ml_end) {
-      a.ml_state[i - a.i0] = (uint32_t)pos | (s << 29);
+      a.ml[i - a.i0] = make_uint2(p, (uint32_t)pos | (s << 29));
     } else {
       const uint64_t d = pos / a.WS;
       if (d < a.nwaves) {
