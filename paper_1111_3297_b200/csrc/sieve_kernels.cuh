@@ -980,6 +980,31 @@ __device__ __forceinline__ uint32_t stage_far(uint32_t cnt_addr, uint32_t ent_ad
 __device__ __forceinline__ void st_rank(uint32_t addr, uint32_t r) {
   asm volatile("st.shared.u16 [%0], %1;" : : "r"(addr), "r"(r) : "memory");
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
+// if (key != kNoRec) *addr = key
+__device__ __forceinline__ void sts_if_rec(uint32_t addr, uint32_t key) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, -1; @q st.shared.u32 [%0], %1; }" : : "r"(addr), "r"(key)
+               : "memory");
+}
 
 template <int NW, int SL, bool FAR>
 __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterArgs& a, uint32_t n) {
@@ -1014,19 +1039,24 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
   }
   __syncthreads();
   const uint32_t shift = a.log_s, smask = (1u << shift) - 1;
+  const uint32_t off_a = smem_addr(sm.off), srt_a = smem_addr(sm.srt), gofs_a = smem_addr(sm.gofs);
   {
-    const uint32_t* rg = sm.reg + warp * Sm::RS;
-    const uint16_t* rk = sm.rank + warp * Sm::RS;
+    // placement in tile order (sentinels of idle lanes are skipped)
+    const uint32_t rg_a = smem_addr(sm.reg + warp * Sm::RS), rk_a = smem_addr(sm.rank + warp * Sm::RS);
+#pragma unroll 2
     for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t key = rg[i];
-      if (key != kNoRec) sm.srt[sm.off[key >> shift] + rk[i]] = key;
+      const uint32_t key = lds_u32(rg_a + 4 * i);
+      const uint32_t o = lds_u32(off_a + 4 * ((key >> shift) & (kScBins - 1)));
+      sts_if_rec(srt_a + 4 * (o + lds_u16(rk_a + 2 * i)), key);
     }
   }
   if constexpr (FAR) {
     const uint32_t base = warp * Sm::FR;
+    const uint32_t fs_a = smem_addr(sm.fslot + base), fr_a = smem_addr(sm.frank + base),
+                   fe_a = smem_addr(sm.freg + base), fg_a = smem_addr(sm.fgofs);
     for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t t = sm.fslot[base + i];
-      if (t != kNoSlot) a.far_buckets[sm.fgofs[t] + sm.frank[base + i]] = sm.freg[base + i];
+      const uint32_t t = lds_u8(fs_a + i);
+      if (t != kNoSlot) a.far_buckets[lds_u32(fg_a + 4 * t) + lds_u16(fr_a + 2 * i)] = lds_u64(fe_a + 8 * i);
     }
   }
   for (uint32_t b = tid; b < nb; b += NT) {
@@ -1035,9 +1065,10 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
   }  // (the sinks are never read: their counts may wrap)
   __syncthreads();
   const uint32_t total = sm.total;
+#pragma unroll 2
   for (uint32_t i = tid; i < total; i += NT) {
-    const uint32_t key = sm.srt[i];
-    a.hits[sm.gofs[key >> shift] + i] = key & smask;
+    const uint32_t key = lds_u32(srt_a + 4 * i);
+    a.hits[lds_u32(gofs_a + 4 * (key >> shift)) + i] = key & smask;
   }
   // off/gofs/srt are rewritten only after the next round's first barrier
 }
@@ -1057,7 +1088,10 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #ifndef EG_FAR_STEPS
 #define EG_FAR_STEPS 6
 #endif
-constexpr int kMlWarps = EG_ML_WARPS, kMlSteps = EG_ML_STEPS;
+#ifndef EG_ML_PF
+#define EG_ML_PF 1
+#endif
+constexpr int kMlWarps = EG_ML_WARPS, kMlSteps = EG_ML_STEPS, kMlPf = EG_ML_PF;
 constexpr int kFarWarps = EG_FAR_WARPS, kFarSteps = EG_FAR_STEPS;
 using MlSmem = ScSmem<kMlWarps, kMlSteps, false>;
 using FarSmem = ScSmem<kFarWarps, kFarSteps, true>;
@@ -1095,16 +1129,15 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
   uint32_t p = e0.x, y = e0.y;
   uint32_t pos = ok ? (y & 0x1fffffffu) : B, s = y >> 29;
   uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
-  // the next unit's primes and states are in flight
-  uint32_t np = 0, ny = 0;
-  {
-    const uint32_t j = (u + nw) * 32 + lane;
-    if (u + nw < nu && j < a.nml) {
-      const uint2 e = a.ml[j];
-      np = e.x;
-      ny = e.y;
-    }
-  }
+  // the next kMlPf units' primes and states are in flight (a sparse unit
+  // takes only a few steps, far less than a DRAM round trip)
+  auto load = [&](uint32_t uu) -> uint2 {
+    const uint32_t j = uu * 32 + lane;
+    return (uu < nu && j < a.nml) ? a.ml[j] : make_uint2(0, 0);
+  };
+  uint2 pf[kMlPf];
+#pragma unroll
+  for (int k = 0; k < kMlPf; ++k) pf[k] = load(u + (k + 1) * nw);
   bool live = u < nu;  // warp-uniform
   for (;;) {
     bool rk_pend = false;  // the last staged rank is stored one step late
@@ -1129,18 +1162,13 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
         }
         idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = np;
-        pos = ok ? (ny & 0x1fffffffu) : B;
-        s = ny >> 29;
+        p = pf[0].x;
+        pos = ok ? (pf[0].y & 0x1fffffffu) : B;
+        s = pf[0].y >> 29;
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
-        const uint32_t j = (u + nw) * 32 + lane;
-        np = 0;
-        ny = 0;
-        if (u + nw < nu && j < a.nml) {
-          const uint2 e = a.ml[j];
-          np = e.x;
-          ny = e.y;
-        }
+#pragma unroll
+        for (int k = 0; k + 1 < kMlPf; ++k) pf[k] = pf[k + 1];
+        pf[kMlPf - 1] = load(u + kMlPf * nw);
         continue;
       }
 #if EG_ML_COMPACT
