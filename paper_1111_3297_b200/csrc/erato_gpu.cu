@@ -85,6 +85,7 @@ uint64_t pi_upper(uint64_t x) {
 
 constexpr uint32_t kBaseLogTile = 20;  // tile size for the sieve of [1, sqrt(v)]
 constexpr uint32_t kGenBlocksPerSm = 2;
+constexpr uint64_t kFewLarge = 2048;  // at most this many primes > S are sieved as medium primes
 
 }  // namespace
 
@@ -416,13 +417,18 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     CUDA_TRY(cudaMemcpyAsync(hb, d_scal, sizeof(hb), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const uint64_t nprimes = hb[0];
-    const uint64_t i61 = hb[8], iwarp = std::max(hb[9], hb[8]), iS = hb[10], iWS = hb[11];
-    const uint64_t idense = std::max(hb[12], iS);
     if (nprimes > c->max_base_pairs)
       return fail(ERATO_GPU_ALLOC_LIMIT, std::to_string(nprimes) + " base primes exceed cap " +
                                               std::to_string(c->max_base_pairs));
     uint32_t pmax = 0;
     if (nprimes) CUDA_TRY(cudaMemcpy(&pmax, c->primes.as<uint32_t>() + nprimes - 1, 4, cudaMemcpyDeviceToHost));
+    // A handful of primes just above the tile size (cfg3: 37) are cheaper as
+    // medium primes (a per-tile start offset each) than through the scatter,
+    // whose per-wave cost is mostly fixed.
+    const bool few_large = nprimes - hb[10] <= kFewLarge && pmax < (1u << 24);
+    const uint64_t i61 = hb[8], iwarp = std::max(hb[9], hb[8]);
+    const uint64_t iS = few_large ? nprimes : hb[10], iWS = std::max(hb[11], iS);
+    const uint64_t idense = std::max(hb[12], iS);
 
     // ---------------- 4. medium constants + large-prime structures ----------------
     const uint64_t nmed = iS - i61, nml = iWS - iS, nfar = nprimes - iWS;
@@ -559,10 +565,15 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml, eg::kMlWarps * 32,
                                                              sizeof(eg::MlSmem)));
-      ml_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
+      // no more CTAs than units of work (small runs: a handful of ML primes)
+      const uint64_t ml_units = (nml + 31) / 32;
+      ml_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+                                               std::max<uint64_t>(1, (ml_units + eg::kMlWarps - 1) / eg::kMlWarps));
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_far, eg::kFarWarps * 32,
                                                              sizeof(eg::FarSmem)));
-      far_blocks = (uint32_t)c->nsm * (uint32_t)std::max(occ, 1);
+      const uint64_t far_units = (std::min<uint64_t>(nfar, bcap) + 31) / 32;  // bucket size bound
+      far_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+                                                std::max<uint64_t>(1, (far_units + eg::kFarWarps - 1) / eg::kFarWarps));
     }
     if (have_large) {
       sca.ml = ga.ml;
