@@ -240,8 +240,9 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   c->nsm = prop.multiProcessorCount;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
-  CUDA_TRY(cudaFuncSetAttribute(eg::k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
+  for (auto kt : {eg::k_tile<false>, eg::k_tile<true>})
+    CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_ml, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -288,9 +289,23 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
 namespace {
 
 // Launch the tile kernel over `ntiles` tiles starting at `tile0`.
-void launch_tiles(erato_gpu_ctx* c, cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles) {
+// p2: multiples from p^2 on (overlap runs, base sieve).
+void launch_tiles(cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles, bool p2) {
   const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8 + (size_t)a.nmed_warp * 8;
-  eg::k_tile<<<ntiles, eg::kTileThreads, smem, st>>>(a);
+  if (p2) eg::k_tile<true><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+  else eg::k_tile<false><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+}
+
+// Split of the group-per-prime medium primes (indices [0, nwarp) of the
+// medium list, ascending p): counts for 32-lane (p < S/256) and 16-lane
+// (p < S/128) groups, from the list indices of those bounds.
+#ifndef EG_GROUPS
+#define EG_GROUPS 1
+#endif
+void group_split(eg::TileArgs& ta, uint64_t i256, uint64_t i128) {
+  if (!EG_GROUPS) i256 = i128 = ta.nmed_warp;  // 32-lane groups only
+  ta.nmed_g32 = (uint32_t)std::min<uint64_t>(i256, ta.nmed_warp);
+  ta.nmed_g16 = (uint32_t)std::min<uint64_t>(std::max(i128, i256), ta.nmed_warp) - ta.nmed_g32;
 }
 
 // Sorted list of the zero bits of bits[0..nbits) at indices >= lo, as base + 2*j.
@@ -352,7 +367,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
   {
     int occ = 1;
     const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8 + eg::kMaxWarpPrimes * 8;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile, eg::kTileThreads, smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile<false>, eg::kTileThreads, smem));
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
     W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
@@ -390,16 +405,19 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       ta.med = c->spm.as<uint4>() + b61;
       ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
       {
-        const auto bw = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), (1u << kBaseLogTile) / 64) - c->h_sp.begin();
-        ta.nmed_warp = (uint32_t)std::min<int64_t>(std::min<int64_t>(std::max<int64_t>(bw - b61, 0), ta.nmed),
-                                                   eg::kMaxWarpPrimes);
+        auto idx_below = [&](uint32_t x) {  // medium-list index of the first prime >= x
+          const int64_t i = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), x) - c->h_sp.begin();
+          return (uint64_t)std::max<int64_t>(i - b61, 0);
+        };
+        ta.nmed_warp = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(idx_below((1u << kBaseLogTile) / 64), ta.nmed),
+                                                    eg::kMaxWarpPrimes);
+        group_split(ta, idx_below((1u << kBaseLogTile) / 256), idx_below((1u << kBaseLogTile) / 128));
       }
       ta.ptab = c->ptab.as<uint32_t>();
       ta.table = c->base_bits.as<uint32_t>();
       ta.count = reinterpret_cast<unsigned long long*>(d_scal + 20);
-      ta.p2_floor = 1;
       const uint64_t bt = (nbase_bits + (1u << kBaseLogTile) - 1) >> kBaseLogTile;
-      launch_tiles(c, st, ta, (uint32_t)bt);
+      launch_tiles(st, ta, (uint32_t)bt, true);
       ++launches;
       rc = compact_zeros<uint32_t>(c, st, c->base_bits.as<uint32_t>(), nbase_bits, 1, 1, c->primes.as<uint32_t>(),
                                    prime_cap, d_scal + 0);
@@ -409,11 +427,13 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
     }
     // ---------------- 3. class boundaries (one host sync) ----------------
-    uint64_t thr[5] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(P.WS / 8, P.S)};
+    // index of the first prime above 61, S/64, S, WS, max(WS/8, S), S/256, S/128
+    uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(P.WS / 8, P.S), (uint64_t)P.S / 256,
+                       (uint64_t)P.S / 128};
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
-    eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 5, d_scal + 8);
+    eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 7, d_scal + 8);
     ++launches;
-    uint64_t hb[13];
+    uint64_t hb[15];
     CUDA_TRY(cudaMemcpyAsync(hb, d_scal, sizeof(hb), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const uint64_t nprimes = hb[0];
@@ -504,13 +524,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     ta.med = c->med.as<uint4>();
     ta.nmed = (uint32_t)nmed;
     ta.nmed_warp = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(iwarp - i61, nmed), eg::kMaxWarpPrimes);
+    group_split(ta, std::max(hb[13], i61) - i61, std::max(hb[14], i61) - i61);
     ta.ptab = c->ptab.as<uint32_t>();
     ta.hits = have_large ? c->hits.as<uint32_t>() : nullptr;
     ta.hitcnt = c->hitcnt.as<uint32_t>();
     ta.hcap = hcap;
     ta.table = static_cast<uint32_t*>(dev_table);
     ta.count = d_count;
-    ta.p2_floor = P.overlap ? 1 : 0;
+    ta.tbase = 0;
     const uint32_t gen_blocks = (uint32_t)c->nsm * kGenBlocksPerSm;
     const uint32_t gen_warps = gen_blocks * (eg::kGenThreads / 32);
     const uint32_t bin_blocks = std::max<uint32_t>((uint32_t)c->nsm * 2, (gen_warps + eg::kMaxRegionsPerCta - 1) / eg::kMaxRegionsPerCta);
@@ -640,8 +661,16 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
       }
       ta.tile0 = tile0;
+      if (tile0 + ntw - ta.tbase > eg::kMaxChunkTiles && nmed) {
+        // new chunk: medium records for tile indices relative to tile0 (< 2^22)
+        ta.tbase = tile0;
+        eg::k_med_records<<<(unsigned)((nmed + 255) / 256), 256, 0, st>>>(
+            c->primes.as<uint32_t>() + i61, (uint32_t)nmed, 2 * (P.g0 + (tile0 << P.log_s)) + 1, P.log_s,
+            c->med.as<uint4>());
+        ++launches;
+      }
       if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
-      launch_tiles(c, st, ta, ntw);
+      launch_tiles(st, ta, ntw, P.overlap);
       if (timing) {
         CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
         ev_pairs.push_back({evi, false});

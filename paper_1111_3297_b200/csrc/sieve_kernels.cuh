@@ -106,9 +106,10 @@ __device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t minv, uint64_
 // step = one entry step).  Bit b of entry c is set iff (32c+b) = (p-1)/2
 // (mod p) for a p of the group (masks.hpp:4-12).
 constexpr int kNumGroups = 8;
-constexpr uint32_t kPatWords = 10240;  // 10238 rounded to a multiple of 4
+constexpr uint32_t kPatPad = 96;        // wrap-around entries per group (4 windows 32 apart)
+constexpr uint32_t kPatWords = 11008;  // sum of (M + 96), rounded to a multiple of 4
 __constant__ uint32_t c_gmod[kNumGroups] = {105, 143, 323, 667, 1147, 1763, 2491, 3599};
-__constant__ uint32_t c_goff[kNumGroups] = {0, 105, 248, 571, 1238, 2385, 4148, 6639};
+__constant__ uint32_t c_goff[kNumGroups] = {0, 201, 440, 859, 1622, 2865, 4724, 7311};  // M + 96 each
 __constant__ uint32_t c_ginv32[kNumGroups] = {23, 76, 212, 271, 466, 1157, 1012, 1912};
 __constant__ uint8_t c_gprimes[kNumGroups][3] = {{3, 5, 7},   {11, 13, 0}, {17, 19, 0}, {23, 29, 0},
                                                  {31, 37, 0}, {41, 43, 0}, {47, 53, 0}, {59, 61, 0}};
@@ -120,11 +121,12 @@ __global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
   int k = kNumGroups - 1;
   while (k > 0 && i < c_goff[k]) --k;
   const uint32_t M = c_gmod[k];
-  const uint32_t c = i - c_goff[k];
-  if (c >= M) {  // padding words
+  uint32_t c = i - c_goff[k];
+  if (c >= M + kPatPad) {  // alignment padding after the last group
     ptab[i] = 0;
     return;
   }
+  if (c >= M) c -= M;  // wrap-around entries
   uint32_t w = 0;
   for (uint32_t b = 0; b < 32; ++b) {
     const uint32_t x = (32u * c + b) % M;
@@ -137,29 +139,28 @@ __global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
 }
 
 // ---------------------------------------------------------------------------
-// Medium-prime record, one per prime per run (16 B, read by every tile):
-//   x    p | inv30(p) << 24         (p < 2^24; inv30 = p^-1 mod 30)
-//   y    r0  = (2*g0 + 1) mod p     (residue of the run's first odd number)
-//   z    rho = (2*S) mod p          (residue step per tile)
-//   w    float 1/p                  (quotient estimate for (t*rho) mod p)
-// Tile t then needs only 32-bit work: r_t = (r0 + t*rho) mod p gives the
-// first multiple c*p >= x_t = 2*(g0 + t*S) + 1, and the cofactor class is
-// c = (x_t + d) * p^-1 (mod 30) — no 64-bit division per (prime, tile).
-struct MedRecs {
-  const uint4* rec;
-  uint32_t n;
-};
+// Medium-prime record, one per prime per chunk of tiles (16 B, read by
+// every tile), M = 30p (one wheel period of cofactors):
+//   x    p                          (p < 2^24)
+//   y    R0  = x_0 mod M            (x_0 = first odd number of the chunk)
+//   z    rho = (2*S) mod M          (residue step per tile)
+//   w    float 1/p
+// Tile t of the chunk starts at x_t = x_0 + 2*S*t with R_t = x_t mod M =
+// (R0 + t*rho) mod M (fp32 quotient estimate, 32-bit wrap-around remainder,
+// t < 2^22).  The first multiple c*p >= x_t has c = 30k + ceil(R_t/p), so
+// c' = ceil(R_t/p) in [0, 30] alone gives the first wheel-admissible
+// cofactor (table combo[c']) and its offset (c'+adv)*p - R_t: Lemma 1
+// (first_offset, src/wheel.cpp:43-47) and wheel_align (src/wheel.cpp:60-69)
+// per (prime, tile) without 64-bit division.
+constexpr uint32_t kMaxChunkTiles = 1u << 22;
 
 __global__ void k_med_records(const uint32_t* __restrict__ primes, uint32_t n, uint64_t x0, uint32_t log_s,
                               uint4* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t p = primes[i];
-  const uint32_t pm = p % 30u;
-  // p^-1 mod 30 for the 8 residues coprime to 30
-  const uint32_t inv = pm == 1 ? 1 : pm == 7 ? 13 : pm == 11 ? 11 : pm == 13 ? 7 : pm == 17 ? 23 : pm == 19 ? 19
-                     : pm == 23 ? 17 : 29;
-  out[i] = make_uint4(p | (inv << 24), (uint32_t)(x0 % p), (uint32_t)(((uint64_t)2 << log_s) % p),
+  const uint32_t M = 30u * p;
+  out[i] = make_uint4(p, (uint32_t)(x0 % M), (uint32_t)(((uint64_t)2 << log_s) % M),
                       __float_as_uint(1.0f / (float)p));
 }
 
@@ -170,10 +171,12 @@ struct TileArgs {
   uint64_t g0;     // global odd index of table bit 0 (= f << l)
   uint64_t tbits;  // table bits T of this run (shard)
   uint64_t tile0;  // first tile of this launch
+  uint64_t tbase;  // first tile of the chunk the medium records were made for
   uint32_t log_s;
   const uint4* med;      // medium-prime records (61 < p <= S), ascending p
   uint32_t nmed;
-  uint32_t nmed_warp;    // the first nmed_warp medium primes are marked warp-per-prime
+  uint32_t nmed_warp;    // the first nmed_warp medium primes (p < S/64) are marked group-per-prime:
+  uint32_t nmed_g32, nmed_g16;  // the first nmed_g32 by 32 lanes (p < S/256), the next nmed_g16 by 16
   const uint32_t* ptab;  // kPatWords pattern words (global)
   const uint32_t* hits;  // [gridDim.x][hcap] hit offsets (large primes), may be null
   uint32_t* hitcnt;      // [gridDim.x], zeroed after use
@@ -181,51 +184,58 @@ struct TileArgs {
   uint32_t* table;               // output words (nullable: count only)
   unsigned long long* count;     // zero-bit accumulator
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
-  int p2_floor;                  // 1: multiples from p^2 (overlap runs, base sieve)
 };
 
-#ifndef EG_TILE_DYNAMIC
-#define EG_TILE_DYNAMIC 0
-#endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 4096;  // medium primes below S/64 (1900 at S = 2^20)
 constexpr int kTileWarps = kTileThreads / 32;
 
 __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
 
-// First admissible multiple of a medium prime in tile t (see MedRecs).
-// Returns the index offset from the tile start (may be >= S) and class s.
-__device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, uint32_t X30, uint64_t x_t,
-                                              bool early, const uint8_t* combo, uint32_t& p, uint32_t& s) {
-  p = rec.x & 0xffffffu;
-  const uint32_t inv30 = rec.x >> 24;
-  // (t * rho) mod p with an fp32 quotient estimate (|error| <= 2)
-  const uint32_t qe = (uint32_t)__fmul_rz(__uint2float_rz(t), __fmul_rz(__uint2float_rz(rec.z), __uint_as_float(rec.w)));
-  int32_t rem = (int32_t)(t * rec.z - qe * p);
-  if (rem < 0) rem += p;
-  if (rem >= (int32_t)p) rem -= p;
-  if (rem >= (int32_t)p) rem -= p;
-  uint32_t r = rec.y + (uint32_t)rem;
-  if (r >= p) r -= p;
-  uint32_t d = r ? p - r : 0;  // c1*p - x_t, c1 = ceil(x_t/p)
-  if (early && x_t + d < (uint64_t)p * p) {  // p^2 floor (overlap runs); far floors only need q0 >= S
+// First wheel-admissible multiple of a medium prime in tile t of the chunk
+// (see k_med_records): index offset from the tile start (may be >= S) and
+// the cofactor class s.  P2: multiples from p^2 on (overlap runs and the
+// base sieve, where the primes themselves lie inside the interval).
+template <bool P2>
+__device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, float tf, uint64_t x_t,
+                                              const uint8_t* combo, uint32_t& p, uint32_t& s) {
+  p = rec.x;
+  const uint32_t M = 30u * p;
+  const float w = __uint_as_float(rec.w);
+  const uint32_t qe = __float2uint_rz(tf * __uint2float_rz(rec.z) * w * (1.0f / 30.0f));
+  int32_t rem = (int32_t)(t * rec.z - qe * M);  // (t*rho) mod M, off by at most one M
+  rem += rem < 0 ? (int32_t)M : 0;
+  rem -= rem >= (int32_t)M ? (int32_t)M : 0;
+  uint32_t R = rec.y + (uint32_t)rem;
+  R -= R >= M ? M : 0;
+  uint32_t c = __float2uint_ru(__uint2float_rz(R) * w);  // ceil(R/p), off by at most one
+  int32_t e = (int32_t)(c * p - R);
+  if (e < 0) {
+    ++c;
+    e += (int32_t)p;
+  } else if (e >= (int32_t)p) {
+    --c;
+    e -= (int32_t)p;
+  }
+  const uint32_t cb = combo[c];
+  uint32_t d = (uint32_t)e + (cb & 7u) * p;  // c_adm * p - x_t
+  s = cb >> 3;
+  if (P2 && x_t + d < (uint64_t)p * p) {  // cofactor p: p^2 (admissible, class of p mod 30)
     const uint64_t dd = (uint64_t)p * p - x_t;
     d = dd < (1u << 30) ? (uint32_t)dd : (1u << 30);
+    s = combo[32 + p % 30u];
   }
-  const uint32_t cm = ((X30 + d % 30u) * inv30) % 30u;
-  const uint32_t cb = combo[cm];
-  s = cb >> 3;
-  return (d + (cb & 7u) * p) >> 1;
+  return d >> 1;
 }
 
+template <bool P2>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   extern __shared__ uint4 smem4[];
   uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
   uint32_t* const tile = pat + kPatWords;
   uint2* const s_wq = reinterpret_cast<uint2*>(tile + ((1u << a.log_s) >> 5));  // [nmed_warp] (q0, p | s<<29)
-  __shared__ uint32_t s_item;
   __shared__ unsigned long long s_red[kTileWarps];
-  __shared__ uint8_t s_combo[32];
+  __shared__ uint8_t s_combo[64];  // [c'] = adv | cls << 3 (c' = 0..30); [32 + r] = cls of r
   __shared__ uint32_t s_cum[8];
 
   const uint32_t tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
@@ -238,35 +248,50 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   {  // stage pattern tables and the wheel tables
     const uint4* src = reinterpret_cast<const uint4*>(a.ptab);
     for (uint32_t i = tid; i < kPatWords / 4; i += bd) smem4[i] = src[i];
-    if (tid < 30) s_combo[tid] = (uint8_t)(c_adv[tid] | (c_cls[tid + c_adv[tid]] << 3));
+    if (tid < 31) {
+      const uint32_t r = tid % 30u;
+      s_combo[tid] = (uint8_t)(c_adv[r] | (c_cls[r + c_adv[r]] << 3));
+    } else if (tid >= 32 && tid < 62) {
+      s_combo[tid] = c_cls[tid - 32];
+    }
     if (tid < 8) {
       uint32_t v = 0;
       for (int k = 0; k < 8; ++k) v |= (uint32_t)c_cum[tid][k] << (4 * k);
       s_cum[tid] = v;
     }
-    if (tid == 0) s_item = 0;
   }
   __syncthreads();
 
-  // 1. small primes: OR of the 8 group windows, plain stores
+  // 1. small primes: OR of the 8 group windows.  Lane l of a warp builds
+  // words l, l+32, l+64, l+96 of the warp's 128-word block: one phase
+  // update per 4 words, conflict-free loads (each group table is padded by
+  // 96 entries, so the 4 windows never wrap).
   {
+    constexpr uint32_t kBlock = 128, kStride = kTileWarps * kBlock;
     uint32_t cur[kNumGroups], stp[kNumGroups];
 #pragma unroll
     for (int k = 0; k < kNumGroups; ++k) {
       const uint32_t M = c_gmod[k];
       const uint32_t cg = (uint32_t)((g % M) * c_ginv32[k] % M);
-      cur[k] = (cg + tid) % M;
-      stp[k] = bd % M;
+      cur[k] = (cg + warp * kBlock + lane) % M;
+      stp[k] = kStride % M;
     }
-    for (uint32_t w = tid; w < nw; w += bd) {
-      uint32_t v = 0;
+    for (uint32_t w = warp * kBlock + lane; w < nw; w += kStride) {
+      uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
 #pragma unroll
       for (int k = 0; k < kNumGroups; ++k) {
-        v |= pat[c_goff[k] + cur[k]];
+        const uint32_t* src = pat + c_goff[k] + cur[k];
+        v0 |= src[0];
+        v1 |= src[32];
+        v2 |= src[64];
+        v3 |= src[96];
         cur[k] += stp[k];
         if (cur[k] >= c_gmod[k]) cur[k] -= c_gmod[k];
       }
-      tile[w] = v;
+      tile[w] = v0;
+      tile[w + 32] = v1;
+      tile[w + 64] = v2;
+      tile[w + 96] = v3;
     }
   }
   __syncthreads();
@@ -282,34 +307,45 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   // 2. medium primes
   {
     const uint64_t x_t = 2 * g + 1;
-    const uint32_t X30 = (uint32_t)(x_t % 30u);
-    const uint32_t t = (uint32_t)t64;
-    const bool early = a.p2_floor && x_t < ((uint64_t)1 << 42);
-    // 2a. warp-per-prime (p < S/64): start offsets computed lane-parallel into
-    // shared memory, then each warp takes one prime at a time (dynamic, largest
-    // work first); lane j marks wheel class (s+j)&7 of period j>>3 (32 lanes =
-    // 4 periods = 60p).
+    const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^22)
+    const float tf = __uint2float_rz(t);
+    // 2a. group-per-prime (p < S/64): start offsets computed lane-parallel
+    // into shared memory; then a group of G lanes takes one prime, lane j
+    // marking wheel class (s+j)&7 of period j>>3 (step G/8 wheel periods):
+    // G = 32 for p < S/256, 16 below S/128, 8 below S/64 — every lane makes
+    // at least ~4 marks.
     for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
       uint32_t p, s;
-      const uint32_t q0 = med_first(a.med[i], t, X30, x_t, early, s_combo, p, s);
+      const uint32_t q0 = med_first<P2>(a.med[i], t, tf, x_t, s_combo, p, s);
       s_wq[i] = make_uint2(q0, p | (s << 29));
     }
     __syncthreads();
-#if EG_TILE_DYNAMIC
-    for (;;) {
-      uint32_t item = 0;
-      if (lane == 0) item = atomicAdd(&s_item, 1u);
-      item = __shfl_sync(kFull, item, 0);
-      if (item >= a.nmed_warp) break;
-#else
+    const uint32_t n32 = a.nmed_g32, n16 = a.nmed_g16, i16 = (n16 + 1) >> 1;
+    const uint32_t nitems = n32 + i16 + (a.nmed_warp - n32 - n16 + 3) / 4;
     // static round-robin (no barrier follows: the lane-per-prime phase
     // absorbs the imbalance)
-    for (uint32_t item = warp; item < a.nmed_warp; item += kTileWarps) {
-#endif
-      const uint2 w = s_wq[item];
+    for (uint32_t item = warp; item < nitems; item += kTileWarps) {
+      uint32_t idx, j, lim, shp;  // prime, lane in group, end of the group's class, log2(G/8)
+      if (item < n32) {
+        idx = item;
+        j = lane;
+        lim = n32;
+        shp = 2;
+      } else if (item < n32 + i16) {
+        idx = n32 + 2 * (item - n32) + (lane >> 4);
+        j = lane & 15;
+        lim = n32 + n16;
+        shp = 1;
+      } else {
+        idx = n32 + n16 + 4 * (item - n32 - i16) + (lane >> 3);
+        j = lane & 7;
+        lim = a.nmed_warp;
+        shp = 0;
+      }
+      const uint2 w = s_wq[idx < lim ? idx : 0];
       const uint32_t p = w.y & 0x1fffffffu, s = w.y >> 29;
-      uint32_t q = w.x + p * (nib(s_cum[s], lane & 7) + 15u * (lane >> 3));
-      const uint32_t step = 60u * p;
+      uint32_t q = idx < lim ? w.x + p * (nib(s_cum[s], j & 7) + 15u * (j >> 3)) : S;
+      const uint32_t step = (15u * p) << shp;
       for (; q + 3 * step < S; q += 4 * step) {
         mark(tile, q);
         mark(tile, q + step);
@@ -318,7 +354,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       }
       for (; q < S; q += step) mark(tile, q);
     }
-    // 2b. lane-per-prime (S/64 <= p <= S): whole wheel periods unrolled for
+    // 2b. lane-per-prime (S/64 <= p): whole wheel periods unrolled for
     // p <= S/8, a plain wheel walk for the few-mark primes above
     const uint32_t nlane = a.nmed - a.nmed_warp;
     const uint32_t nitem = (nlane + 31) / 32;
@@ -332,7 +368,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       if (nx < nitem && nx * 32 + lane < nlane) rec = a.med[a.nmed_warp + nx * 32 + lane];
       if (valid) {
         uint32_t p, s;
-        uint32_t q = med_first(cur, t, X30, x_t, early, s_combo, p, s);
+        uint32_t q = med_first<P2>(cur, t, tf, x_t, s_combo, p, s);
         if ((p << 3) > S) {
           while (q < S) {
             mark(tile, q);
