@@ -251,7 +251,7 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
                                 (int)sizeof(eg::FarSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
-  CUDA_TRY(c->spm.ensure(8192 * 16));
+  CUDA_TRY(c->spm.ensure((8192 + eg::kMedPad) * 16));
   CUDA_TRY(c->ptab.ensure(eg::kPatWords * 4));
   CUDA_TRY(c->scal.ensure(64 * 8));
   eg::k_build_patterns<<<(eg::kPatWords + 255) / 256, 256, 0, c->stream>>>(c->ptab.as<uint32_t>());
@@ -452,7 +452,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
 
     // ---------------- 4. medium constants + large-prime structures ----------------
     const uint64_t nmed = iS - i61, nml = iWS - iS, nfar = nprimes - iWS;
-    CUDA_TRY(c->med.ensure(std::max<uint64_t>(nmed, 1) * 16));
+    CUDA_TRY(c->med.ensure((nmed + eg::kMedPad) * 16));  // padded: the tile kernel prefetches past the end
     if (nmed)
       eg::k_med_records<<<(unsigned)((nmed + 255) / 256), 256, 0, st>>>(c->primes.as<uint32_t>() + i61, (uint32_t)nmed,
                                                                          2 * P.g0 + 1, P.log_s, c->med.as<uint4>());

@@ -46,6 +46,14 @@ namespace eg {
 
 constexpr uint32_t kFull = 0xffffffffu;
 
+// 32-bit shared-memory address of a generic pointer into shared memory
+// (volatile: computed once, not rematerialised inside hot loops).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  uint32_t r;
+  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // mod-30 wheel over odd cofactors c of p*c.  Admissible residues (coprime to
 // 30): R = {1,7,11,13,17,19,23,29}; class s <-> R[s].  In index space the
@@ -144,15 +152,16 @@ __global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
 //   x    p                          (p < 2^24)
 //   y    R0  = x_0 mod M            (x_0 = first odd number of the chunk)
 //   z    rho = (2*S) mod M          (residue step per tile)
-//   w    float 1/p
+//   w    float rho / M
 // Tile t of the chunk starts at x_t = x_0 + 2*S*t with R_t = x_t mod M =
 // (R0 + t*rho) mod M (fp32 quotient estimate, 32-bit wrap-around remainder,
-// t < 2^22).  The first multiple c*p >= x_t has c = 30k + ceil(R_t/p), so
+// t < 2^20).  The first multiple c*p >= x_t has c = 30k + ceil(R_t/p), so
 // c' = ceil(R_t/p) in [0, 30] alone gives the first wheel-admissible
 // cofactor (table combo[c']) and its offset (c'+adv)*p - R_t: Lemma 1
 // (first_offset, src/wheel.cpp:43-47) and wheel_align (src/wheel.cpp:60-69)
 // per (prime, tile) without 64-bit division.
-constexpr uint32_t kMaxChunkTiles = 1u << 22;
+constexpr uint32_t kMaxChunkTiles = 1u << 20;
+constexpr uint32_t kMedPad = 2048;  // records past the end the tile kernel may prefetch
 
 __global__ void k_med_records(const uint32_t* __restrict__ primes, uint32_t n, uint64_t x0, uint32_t log_s,
                               uint4* __restrict__ out) {
@@ -160,8 +169,8 @@ __global__ void k_med_records(const uint32_t* __restrict__ primes, uint32_t n, u
   if (i >= n) return;
   const uint32_t p = primes[i];
   const uint32_t M = 30u * p;
-  out[i] = make_uint4(p, (uint32_t)(x0 % M), (uint32_t)(((uint64_t)2 << log_s) % M),
-                      __float_as_uint(1.0f / (float)p));
+  const uint32_t rho = (uint32_t)(((uint64_t)2 << log_s) % M);
+  out[i] = make_uint4(p, (uint32_t)(x0 % M), rho, __float_as_uint((float)((double)rho / (double)M)));
 }
 
 // combo[cm] = adv | cls << 3 ; cum4[s] = nibbles cum[s][0..7]
@@ -186,6 +195,12 @@ struct TileArgs {
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
 };
 
+#ifndef EG_HIT_PF
+#define EG_HIT_PF 0
+#endif
+#ifndef EG_RP_PF
+#define EG_RP_PF 1
+#endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 4096;  // medium primes below S/64 (1900 at S = 2^20)
 constexpr int kTileWarps = kTileThreads / 32;
@@ -196,34 +211,45 @@ __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&til
 // (see k_med_records): index offset from the tile start (may be >= S) and
 // the cofactor class s.  P2: multiples from p^2 on (overlap runs and the
 // base sieve, where the primes themselves lie inside the interval).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t lds_u8c(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 template <bool P2>
-__device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, float tf, uint64_t x_t,
-                                              const uint8_t* combo, uint32_t& p, uint32_t& s) {
+__device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, float tf, uint64_t x_t, uint32_t combo_a,
+                                              uint32_t& p, uint32_t& s) {
   p = rec.x;
   const uint32_t M = 30u * p;
-  const float w = __uint_as_float(rec.w);
-  const uint32_t qe = __float2uint_rz(tf * __uint2float_rz(rec.z) * w * (1.0f / 30.0f));
-  int32_t rem = (int32_t)(t * rec.z - qe * M);  // (t*rho) mod M, off by at most one M
-  rem += rem < 0 ? (int32_t)M : 0;
-  rem -= rem >= (int32_t)M ? (int32_t)M : 0;
-  uint32_t R = rec.y + (uint32_t)rem;
+  // floor(t*rho/M) or one less (t < 2^20: |fp32 error| < 0.1), so the
+  // 32-bit wrap-around remainder lies in [0, 2M)
+  const uint32_t qe = __float2uint_rz(__fmaf_rn(tf, __uint_as_float(rec.w), -0.5f));
+  uint32_t R = rec.y + (t * rec.z - qe * M);  // R_t in [0, 3M)
   R -= R >= M ? M : 0;
-  uint32_t c = __float2uint_ru(__uint2float_rz(R) * w);  // ceil(R/p), off by at most one
+  R -= R >= M ? M : 0;
+  EG_CHECK(R < M, "med_first R=%u M=%u p=%u t=%u qe=%u rec=(%u,%u,%u,%08x)", R, M, p, t, qe, rec.x, rec.y, rec.z, rec.w);
+  uint32_t c = __float2uint_ru(__uint2float_rz(R) * rcp_approx(__uint2float_rn(p)));  // ceil(R/p) +- 1
   int32_t e = (int32_t)(c * p - R);
-  if (e < 0) {
-    ++c;
-    e += (int32_t)p;
-  } else if (e >= (int32_t)p) {
-    --c;
-    e -= (int32_t)p;
-  }
-  const uint32_t cb = combo[c];
+  const bool lo = e < 0;
+  c += lo ? 1u : 0u;
+  e += lo ? (int32_t)p : 0;
+  const bool hi = e >= (int32_t)p;
+  c -= hi ? 1u : 0u;
+  e -= hi ? (int32_t)p : 0;
+  EG_CHECK(c <= 30 && e >= 0 && e < (int32_t)p, "med_first c=%u e=%d p=%u R=%u", c, e, p, R);
+  const uint32_t cb = lds_u8c(combo_a + c);
   uint32_t d = (uint32_t)e + (cb & 7u) * p;  // c_adm * p - x_t
   s = cb >> 3;
   if (P2 && x_t + d < (uint64_t)p * p) {  // cofactor p: p^2 (admissible, class of p mod 30)
     const uint64_t dd = (uint64_t)p * p - x_t;
     d = dd < (1u << 30) ? (uint32_t)dd : (1u << 30);
-    s = combo[32 + p % 30u];
+    s = lds_u8c(combo_a + 32 + p % 30u);
   }
   return d >> 1;
 }
@@ -307,8 +333,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   // 2. medium primes
   {
     const uint64_t x_t = 2 * g + 1;
-    const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^22)
+    const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^20)
     const float tf = __uint2float_rz(t);
+    const uint32_t combo_a = smem_addr(s_combo);
     // 2a. group-per-prime (p < S/64): start offsets computed lane-parallel
     // into shared memory; then a group of G lanes takes one prime, lane j
     // marking wheel class (s+j)&7 of period j>>3 (step G/8 wheel periods):
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     // at least ~4 marks.
     for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
       uint32_t p, s;
-      const uint32_t q0 = med_first<P2>(a.med[i], t, tf, x_t, s_combo, p, s);
+      const uint32_t q0 = med_first<P2>(a.med[i], t, tf, x_t, combo_a, p, s);
       s_wq[i] = make_uint2(q0, p | (s << 29));
     }
     __syncthreads();
@@ -358,6 +385,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     // p <= S/8, a plain wheel walk for the few-mark primes above
     const uint32_t nlane = a.nmed - a.nmed_warp;
     const uint32_t nitem = (nlane + 31) / 32;
+#if EG_RP_PF
+    // the record array is padded (kMedPad): next item's record in flight
+    const uint4* rp = a.med + a.nmed_warp + warp * 32 + lane;
+    uint4 rec = *rp;
+    for (uint32_t item = warp; item < nitem; item += kTileWarps) {
+      const uint4 cur = rec;
+      const bool valid = item * 32 + lane < nlane;
+      rp += kTileWarps * 32;
+      rec = *rp;
+#else
     uint32_t item = warp;
     uint4 rec = make_uint4(0, 0, 0, 0);
     if (item < nitem && item * 32 + lane < nlane) rec = a.med[a.nmed_warp + item * 32 + lane];
@@ -366,9 +403,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       const bool valid = item * 32 + lane < nlane;
       const uint32_t nx = item + kTileWarps;
       if (nx < nitem && nx * 32 + lane < nlane) rec = a.med[a.nmed_warp + nx * 32 + lane];
+#endif
       if (valid) {
         uint32_t p, s;
-        uint32_t q = med_first<P2>(cur, t, tf, x_t, s_combo, p, s);
+        uint32_t q = med_first<P2>(cur, t, tf, x_t, combo_a, p, s);
         if ((p << 3) > S) {
           while (q < S) {
             mark(tile, q);
@@ -407,8 +445,15 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     const uint32_t* h = a.hits + (uint64_t)blockIdx.x * a.hcap;
     const uint32_t n4 = cnt >> 2;
     const uint4* h4 = reinterpret_cast<const uint4*>(h);
+#if EG_HIT_PF
+    uint4 nxt = tid < n4 ? h4[tid] : make_uint4(0, 0, 0, 0);  // next quad in flight
+    for (uint32_t i = tid; i < n4; i += bd) {
+      const uint4 v = nxt;
+      if (i + bd < n4) nxt = h4[i + bd];
+#else
     for (uint32_t i = tid; i < n4; i += bd) {
       const uint4 v = h4[i];
+#endif
       EG_CHECK(v.x < S && v.y < S && v.z < S && v.w < S, "hit record out of tile %u %u %u %u", v.x, v.y, v.z, v.w);
       mark(tile, v.x);
       mark(tile, v.y);
@@ -426,8 +471,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   // 4. popcount + write-out (count_zeros simd.cpp:18-25, segment_to_bytes
   // driver.cpp:22-27: LSB-first bytes == little-endian words)
   const uint64_t rem = a.tbits - tstart;
-  const uint32_t valid = rem < S ? (uint32_t)rem : S;  // multiple of 16
-  const uint32_t vbytes = valid >> 3;
+  const uint32_t valid = rem < S ? (uint32_t)rem : S;  // multiple of 16 except in the base sieve
+  const uint32_t vbytes = (valid + 7) >> 3;  // the base sieve table may end inside a byte
   unsigned long long ones = 0;
   uint32_t* out = a.table ? a.table + (tstart >> 5) : nullptr;
   for (uint32_t w4 = tid; w4 < (nw >> 2); w4 += bd) {
@@ -981,13 +1026,7 @@ struct ScSmem {
   static_assert(NW * R < 65536, "ranks are 16-bit");
 };
 
-// Shared-memory helpers for the emission loops: 32-bit shared addresses kept
-// in registers (volatile: computed once, not rematerialised in the loop).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  uint32_t r;
-  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
-  return r;
-}
+// Shared-memory helpers for the emission loops (32-bit shared addresses).
 // r = atomicAdd(cnt, 1) and the record store (unconditional: idle lanes
 // count into their sink and stage the sentinel).  The rank r is stored one
 // step later (st_rank), so the atomic's latency overlaps the next step.

@@ -261,3 +261,26 @@ def test_repeat_runs_deterministic(gpu_ctx):
     a, sa = gpu_ctx.table(p)
     b, sb = gpu_ctx.table(p)
     assert sa.prime_count == sb.prime_count and np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("l,f,n,overlap", [(20, 0, 4096, True), (20, 0, 3001, True), (13, 5000, 77, False),
+                                            (20, (1 << 19) - 512, 1024, False), (16, 1 << 30, 9, False)])
+def test_base_prime_count_fresh_context(restated, l, f, n, overlap):
+    """The device base-prime list (odd primes <= isqrt(v)) is exact on a FRESH
+    context, where [1, isqrt v] rarely ends on a byte boundary (a stale
+    buffer from an earlier run must not hide an unwritten last byte)."""
+    import math
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n, allow_overlap=overlap)
+    ctx = E.Context(0)
+    try:
+        st = ctx.count(p)
+    finally:
+        ctx.close()
+    r = math.isqrt(p.v)
+    sieve = np.ones(r + 1, dtype=bool)
+    sieve[:2] = False
+    for i in range(2, math.isqrt(r) + 1):
+        if sieve[i]:
+            sieve[i * i::i] = False
+    assert st.base_primes == int(sieve[3:].sum())
