@@ -505,9 +505,10 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sa.bcap = bcap;
       sa.nwaves = P.nwaves;
       sa.WS = P.WS;
+      sa.inv_ws = 1.0 / (double)P.WS;
       sa.overflow = reinterpret_cast<int*>(d_scal + 17);
       const uint64_t nl = nprimes - iS;
-      eg::k_setup_large<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(sa);
+      eg::k_setup_large<<<(unsigned)((nl + eg::kSetupThreads - 1) / eg::kSetupThreads), eg::kSetupThreads, 0, st>>>(sa);
       ++launches;
     } else {
       CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));

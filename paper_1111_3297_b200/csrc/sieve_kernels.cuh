@@ -80,21 +80,24 @@ __device__ __forceinline__ uint32_t mod30_u64(uint64_t c) {
 
 // First wheel-admissible multiple p*c >= x with c >= cmin, for odd x = 2g+1
 // (g = global odd index of the tile start).  Returns its index offset from g,
-// (c*p - x)/2, and the wheel class s of c.  minv = floor((2^64-1)/p).
-// Restates Lemma 1 / first_offset (src/wheel.cpp:43-47) plus wheel_align
-// (src/wheel.cpp:60-69) for 64-bit starts without a 128-bit remainder.
-__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t minv, uint64_t x, uint64_t cmin,
-                                              uint32_t& s) {
-  uint64_t c = __umul64hi(x, minv);  // floor(x/p) - {0,1,2}
-  uint64_t r = x - c * p;
-  while (r >= p) {
+// (c*p - x)/2, and the wheel class s of c.  Restates Lemma 1 / first_offset
+// (src/wheel.cpp:43-47) plus wheel_align (src/wheel.cpp:60-69) for 64-bit
+// starts: floor(x/p) from an fp64 estimate (off by at most one), then the
+// exact remainder in wrap-around u64 arithmetic.
+__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint32_t& s) {
+  uint64_t c = __double2ull_rz(__dmul_rz(__ull2double_rz(x), __drcp_rn((double)p)));
+  int64_t r = (int64_t)(x - c * p);  // true remainder, in (-p, 2p)
+  if (r < 0) {
+    r += p;
+    --c;
+  } else if (r >= (int64_t)p) {
     r -= p;
     ++c;
   }
   uint64_t d = 0;  // c*p - x after rounding c up
   if (r) {
     ++c;
-    d = p - r;
+    d = p - (uint64_t)r;
   }
   if (c < cmin) {
     d += (cmin - c) * (uint64_t)p;
@@ -1388,10 +1391,6 @@ __global__ void __launch_bounds__(1024) k_small_primes(uint32_t* __restrict__ ou
   if (tid == 1023) *count = s_scan[1023];
 }
 
-__global__ void k_barrett(const uint32_t* __restrict__ p, uint64_t* __restrict__ m, uint32_t n) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) m[i] = ~0ull / p[i];
-}
 
 // ---- compaction of a bit table to the sorted list of its zero bits ---------
 // Block = 1024 words (32768 bits).  Zero bit j (lo <= j < nbits) -> value
@@ -1503,12 +1502,17 @@ struct SetupArgs {
   uint32_t ring, bcap;
   uint64_t nwaves;
   uint32_t WS;
+  double inv_ws;
   int* overflow;
 };
 
-__global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
+constexpr int kSetupThreads = 1024;
+
+__global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a) {
+  __shared__ uint32_t s_cnt[kScBins], s_base[kScBins];
+  for (uint32_t b = threadIdx.x; b < kScBins; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
   const uint64_t i = a.i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t lane = threadIdx.x & 31;
   bool app = false;
   uint32_t slotb = 0;
   uint64_t ne = 0;
@@ -1517,26 +1521,34 @@ __global__ void __launch_bounds__(256) k_setup_large(const SetupArgs a) {
     uint32_t s;
     // cofactor >= 2 (-> >= 7 after the wheel): never marks p itself and
     // keeps the first hit within 3.5p of the interval start in overlap runs
-    const uint64_t pos = first_hit(p, ~0ull / p, a.x0, 2, s);
+    const uint64_t pos = first_hit(p, a.x0, 2, s);
     if (i < a.i_ml_end) {
       a.ml[i - a.i0] = make_uint2(p, (uint32_t)pos | (s << 29));
     } else {
-      const uint64_t d = pos / a.WS;
+      // d = pos / WS: fp64 estimate (pos < 2^40, off by at most one), exact fix
+      uint64_t d = __double2ull_rz(__dmul_rz(__ull2double_rz(pos), a.inv_ws));
+      if (d * a.WS > pos) --d;
+      if ((d + 1) * a.WS <= pos) ++d;
       if (d < a.nwaves) {
         app = true;
-        slotb = (uint32_t)(d % a.ring);
+        slotb = (uint32_t)d % a.ring;
         ne = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
       }
     }
   }
-  const uint32_t part = __ballot_sync(kFull, app);
+  // CTA-level aggregation of the bucket appends: the first hits of all far
+  // primes fall into the first few waves, so per-warp atomics on those few
+  // counters would serialise
+  uint32_t rank = 0;
+  if (app) rank = atomicAdd(&s_cnt[slotb], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < a.ring; b += blockDim.x) {
+    const uint32_t c = s_cnt[b];
+    if (c) s_base[b] = atomicAdd(&a.far_bcount[b], c);
+  }
+  __syncthreads();
   if (app) {
-    const uint32_t grp = __match_any_sync(part, slotb);
-    const uint32_t leader = __ffs(grp) - 1;
-    uint32_t b = 0;
-    if (lane == leader) b = atomicAdd(&a.far_bcount[slotb], (uint32_t)__popc(grp));
-    b = __shfl_sync(grp, b, leader);
-    const uint32_t pos = b + __popc(grp & ((1u << lane) - 1));
+    const uint32_t pos = s_base[slotb] + rank;
     if (pos < a.bcap) a.far_buckets[(uint64_t)slotb * a.bcap + pos] = ne;
     else atomicExch(a.overflow, 1);
   }
