@@ -1179,9 +1179,7 @@ constexpr uint32_t kScTrash = (uint32_t)(MlSmem::R * kMlWarps > FarSmem::R * kFa
 
 __device__ __forceinline__ uint32_t rotr4(uint32_t x) { return __funnelshift_r(x, x, 4); }
 
-__global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs a) {
-  extern __shared__ uint4 smem_raw[];
-  MlSmem& sm = *reinterpret_cast<MlSmem*>(smem_raw);
+__device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, uint32_t nblk, MlSmem& sm) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t t = tid; t < kScBins; t += blockDim.x) sm.cnt[t] = 0;
   __syncthreads();
@@ -1189,7 +1187,7 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
   // walk bound: the wave end, or the end of the last tile in the last wave
   // (the state written back after the last wave is never read)
   const uint32_t B = a.ntiles_w << a.log_s;
-  const uint32_t nw = gridDim.x * kMlWarps;
+  const uint32_t nw = nblk * kMlWarps;
   const uint32_t nu = (a.nml + 31) / 32;
 #if EG_ML_COMPACT
   const uint32_t lt = (1u << lane) - 1;
@@ -1200,7 +1198,7 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
   const uint32_t rank_a = smem_addr(sm.rank + warp * MlSmem::RS + lane);
 #endif
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
-  uint32_t u = blockIdx.x * kMlWarps + warp;
+  uint32_t u = blk * kMlWarps + warp;
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nml;
   uint2 e0 = ok ? a.ml[idx] : make_uint2(0, 0);
@@ -1281,9 +1279,7 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
   }
 }
 
-__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArgs a) {
-  extern __shared__ uint4 smem_raw[];
-  FarSmem& sm = *reinterpret_cast<FarSmem*>(smem_raw);
+__device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, uint32_t nblk, FarSmem& sm) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t t = tid; t < kScBins; t += blockDim.x) {
     sm.cnt[t] = 0;
@@ -1293,7 +1289,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArg
   const uint32_t WS = a.WS, ring = a.ring, shift = a.log_s;
   const uint32_t lim = a.ntiles_w << a.log_s;
   const uint32_t nfar = min(*a.far_in_count, a.bcap);
-  const uint32_t nw = gridDim.x * kFarWarps;
+  const uint32_t nw = nblk * kFarWarps;
   const uint32_t nu = (nfar + 31) / 32;
   const uint64_t left = a.nwaves - a.wave;  // waves from this one to the end
   const uint32_t wofs = warp * FarSmem::R + lane;
@@ -1302,7 +1298,7 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArg
                  frank_a = smem_addr(sm.frank + wofs);
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
   const uint32_t fcnt_a = smem_addr(sm.fcnt), fsink_a = fcnt_a + 4 * (kScBins + lane);
-  uint32_t u = blockIdx.x * kFarWarps + warp;
+  uint32_t u = blk * kFarWarps + warp;
   // the entries of the next two units are in flight (loads issued early)
   auto load = [&](uint32_t uu) -> uint64_t {
     const uint32_t j = uu * 32 + lane;
@@ -1354,6 +1350,15 @@ __global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArg
     sc_flush(sm, a, k * 32);
     if (!more) break;
   }
+}
+
+__global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  scatter_ml(a, blockIdx.x, gridDim.x, *reinterpret_cast<MlSmem*>(smem_raw));
+}
+__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  scatter_far(a, blockIdx.x, gridDim.x, *reinterpret_cast<FarSmem*>(smem_raw));
 }
 
 // ---------------------------------------------------------------------------
