@@ -56,12 +56,13 @@ ROOF = {
 }
 # Hit records of large primes in this implementation (mod-30 wheel, 2^20-bit
 # tiles), tools/roofline_counts.py `ours_large_records`: k_bin moves 8 B per record.
-LARGE_RECORDS = {1: 0, 2: 0, 3: 20_188, 4: 835_065_655, 5: 7_429_219_143}
+# (cfg3's 37 primes just above the tile size are sieved as medium primes: no records)
+LARGE_RECORDS = {1: 0, 2: 0, 3: 0, 4: 835_065_655, 5: 7_429_219_143}
 # ... of which come from far primes (p > WS = 146 tiles), `ours_far_records`
 FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_802_335_964}
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # (profiles/r01_ncu_summary.txt, cfg5 wave 100)
-NCU_TRAFFIC = {5: {"k_scatter_fused": 132.5e6 + 178.7e6, "k_bin": 206.2e6 + 153.1e6, "k_gen": 132.9e6 + 186.5e6, "k_tile": 133.8e6 + 4.5e6}}
+NCU_TRAFFIC = {5: {"k_tile": 134.0e6 + 3.7e6, "k_scatter_ml": 68.5e6 + 110.6e6, "k_scatter_far": 64.4e6 + 42.7e6}}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 R_ATOM_MEASURED = 3.47e12  # smem atomicOr/s per B200, microbench/mb_atomics.cu (profiles/r01_microbench_atomics.log)
 
