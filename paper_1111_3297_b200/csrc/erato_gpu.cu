@@ -240,9 +240,10 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   c->nsm = prop.multiProcessorCount;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
-  for (auto kt : {eg::k_tile<false>, eg::k_tile<true>})
+  for (auto kt : {eg::k_tile<false, false>, eg::k_tile<true, false>, eg::k_tile<false, true>, eg::k_tile<true, true>})
     CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8)));
+                                  (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8 +
+                                        eg::kTileWarps * eg::kHitChunk * 4)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_ml, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -291,9 +292,15 @@ namespace {
 // Launch the tile kernel over `ntiles` tiles starting at `tile0`.
 // p2: multiples from p^2 on (overlap runs, base sieve).
 void launch_tiles(cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles, bool p2) {
-  const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8 + (size_t)a.nmed_warp * 8;
-  if (p2) eg::k_tile<true><<<ntiles, eg::kTileThreads, smem, st>>>(a);
-  else eg::k_tile<false><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+  const size_t smem = eg::kPatWords * 4 + ((size_t)1 << a.log_s) / 8 + (size_t)((a.nmed_warp + 1) & ~1u) * 8 +
+                      (a.hits ? (size_t)eg::kTileWarps * eg::kHitChunk * 4 : 0);
+  if (a.hits) {
+    if (p2) eg::k_tile<true, true><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+    else eg::k_tile<false, true><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+  } else {
+    if (p2) eg::k_tile<true, false><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+    else eg::k_tile<false, false><<<ntiles, eg::kTileThreads, smem, st>>>(a);
+  }
 }
 
 // Split of the group-per-prime medium primes (indices [0, nwarp) of the
@@ -366,8 +373,8 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
   P.ntiles = (P.T + P.S - 1) >> P.log_s;
   {
     int occ = 1;
-    const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8 + eg::kMaxWarpPrimes * 8;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile<false>, eg::kTileThreads, smem));
+    const size_t smem = eg::kPatWords * 4 + (size_t)P.S / 8 + eg::kMaxWarpPrimes * 8 + eg::kTileWarps * eg::kHitChunk * 4;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_tile<false, true>, eg::kTileThreads, smem));
     if (occ < 1) occ = 1;
     uint64_t W = (uint64_t)c->nsm * occ;
     W = std::min<uint64_t>(W, eg::kMaxWaveTiles);

@@ -205,10 +205,17 @@ struct TileArgs {
 #define EG_RP_PF 1
 #endif
 constexpr int kTileThreads = 1024;
-constexpr uint32_t kMaxWarpPrimes = 4096;  // medium primes below S/64 (1900 at S = 2^20)
+constexpr uint32_t kMaxWarpPrimes = 2048;  // medium primes below S/64 (pi(16384) = 1900 at S = 2^20)
+constexpr uint32_t kHitChunk = 256;        // hit records per warp chunk (1 KB of shared staging per warp)
 constexpr int kTileWarps = kTileThreads / 32;
 
 __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" : : "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" : : : "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" : : : "memory"); }
 
 // First wheel-admissible multiple of a medium prime in tile t of the chunk
 // (see k_med_records): index offset from the tile start (may be >= S) and
@@ -257,12 +264,15 @@ __device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, float
   return d >> 1;
 }
 
-template <bool P2>
+// P2: multiples from p^2 (overlap runs, base sieve); HITS: large-prime hit
+// lists to mark (a.hits != null).
+template <bool P2, bool HITS>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   extern __shared__ uint4 smem4[];
   uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
   uint32_t* const tile = pat + kPatWords;
   uint2* const s_wq = reinterpret_cast<uint2*>(tile + ((1u << a.log_s) >> 5));  // [nmed_warp] (q0, p | s<<29)
+  uint4* const s_hits = reinterpret_cast<uint4*>(s_wq + ((a.nmed_warp + 1) & ~1u));  // [warps][kHitChunk/4] if hits
   __shared__ unsigned long long s_red[kTileWarps];
   __shared__ uint8_t s_combo[64];  // [c'] = adv | cls << 3 (c' = 0..30); [32 + r] = cls of r
   __shared__ uint32_t s_cum[8];
@@ -352,6 +362,57 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     __syncthreads();
     const uint32_t n32 = a.nmed_g32, n16 = a.nmed_g16, i16 = (n16 + 1) >> 1;
     const uint32_t nitems = n32 + i16 + (a.nmed_warp - n32 - n16 + 3) / 4;
+    // 3. large primes: this tile's hit records, in chunks of kHitChunk per
+    // warp, fetched by cp.async into the warp's shared staging while the
+    // warp marks medium primes (the DRAM reads overlap the shared-atomic
+    // work instead of forming a phase of their own); every lane marks the
+    // 8 records it copied itself.
+    const uint32_t hcnt = HITS ? min(a.hitcnt[blockIdx.x], a.hcap) : 0;
+    const uint32_t nch = (hcnt + kHitChunk - 1) / kHitChunk;
+    const uint32_t* const hl = HITS ? a.hits + (uint64_t)blockIdx.x * a.hcap : nullptr;
+    const uint32_t hst_a = smem_addr(s_hits + warp * (kHitChunk / 4) + lane);
+    uint32_t ch = warp;  // next chunk of this warp (chunks warp, warp + 32, ...)
+    bool pend = false;
+    auto issue = [&]() {
+      if (HITS && ch < nch) {
+        const uint32_t* src = hl + ch * kHitChunk + 4 * lane;
+        cp_async16(hst_a, src);
+        cp_async16(hst_a + 512, src + 128);
+        cp_async_commit();
+        pend = true;
+      }
+    };
+    auto consume = [&]() {
+      if constexpr (HITS) {
+        if (!pend) return;
+        cp_async_wait_all();
+        const uint4 v0 = s_hits[warp * (kHitChunk / 4) + lane], v1 = s_hits[warp * (kHitChunk / 4) + 32 + lane];
+        const uint32_t i0 = ch * kHitChunk + 4 * lane, i1 = i0 + 128;
+        if (i1 + 3 < hcnt) {
+          mark(tile, v0.x); mark(tile, v0.y); mark(tile, v0.z); mark(tile, v0.w);
+          mark(tile, v1.x); mark(tile, v1.y); mark(tile, v1.z); mark(tile, v1.w);
+        } else {
+          if (i0 < hcnt) mark(tile, v0.x);
+          if (i0 + 1 < hcnt) mark(tile, v0.y);
+          if (i0 + 2 < hcnt) mark(tile, v0.z);
+          if (i0 + 3 < hcnt) mark(tile, v0.w);
+          if (i1 < hcnt) mark(tile, v1.x);
+          if (i1 + 1 < hcnt) mark(tile, v1.y);
+          if (i1 + 2 < hcnt) mark(tile, v1.z);
+          if (i1 + 3 < hcnt) mark(tile, v1.w);
+        }
+        __syncwarp();  // every lane has read its staging before it is refilled
+        pend = false;
+        ch += kTileWarps;
+        issue();
+      }
+    };
+    issue();
+    // one chunk per `every` medium items of this warp
+    const uint32_t my_items = (nitems + (a.nmed - a.nmed_warp + 31) / 32 + kTileWarps - 1) / kTileWarps;
+    const uint32_t my_chunks = (nch + kTileWarps - 1) / kTileWarps;
+    const uint32_t every = my_chunks ? max(1u, my_items / (my_chunks + 1)) : 0xffffffffu;
+    uint32_t since = 0;
     // static round-robin (no barrier follows: the lane-per-prime phase
     // absorbs the imbalance)
     for (uint32_t item = warp; item < nitems; item += kTileWarps) {
@@ -383,6 +444,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         mark(tile, q + 3 * step);
       }
       for (; q < S; q += step) mark(tile, q);
+      if (HITS && ++since >= every) {
+        since = 0;
+        consume();
+      }
     }
     // 2b. lane-per-prime (S/64 <= p): whole wheel periods unrolled for
     // p <= S/8, a plain wheel walk for the few-mark primes above
@@ -439,35 +504,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
           }
         }
       }
+      if (HITS && ++since >= every) {
+        since = 0;
+        consume();
+      }
     }
-  }
-
-  // 3. large primes: this tile's hit records
-  if (a.hits) {
-    const uint32_t cnt = min(a.hitcnt[blockIdx.x], a.hcap);
-    const uint32_t* h = a.hits + (uint64_t)blockIdx.x * a.hcap;
-    const uint32_t n4 = cnt >> 2;
-    const uint4* h4 = reinterpret_cast<const uint4*>(h);
-#if EG_HIT_PF
-    uint4 nxt = tid < n4 ? h4[tid] : make_uint4(0, 0, 0, 0);  // next quad in flight
-    for (uint32_t i = tid; i < n4; i += bd) {
-      const uint4 v = nxt;
-      if (i + bd < n4) nxt = h4[i + bd];
-#else
-    for (uint32_t i = tid; i < n4; i += bd) {
-      const uint4 v = h4[i];
-#endif
-      EG_CHECK(v.x < S && v.y < S && v.z < S && v.w < S, "hit record out of tile %u %u %u %u", v.x, v.y, v.z, v.w);
-      mark(tile, v.x);
-      mark(tile, v.y);
-      mark(tile, v.z);
-      mark(tile, v.w);
-    }
-    for (uint32_t i = (n4 << 2) + tid; i < cnt; i += bd) mark(tile, h[i]);
+    while (HITS && pend) consume();  // this warp's remaining hit chunks
   }
   __syncthreads();
   if (tid == 0) {
-    if (a.hits) a.hitcnt[blockIdx.x] = 0;
+    if (HITS) a.hitcnt[blockIdx.x] = 0;
     if (blockIdx.x == 0 && a.reset_bucket_count) *a.reset_bucket_count = 0;
   }
 
