@@ -379,8 +379,11 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     uint64_t W = (uint64_t)c->nsm * occ;
     W = std::min<uint64_t>(W, eg::kMaxWaveTiles);
 
-    // ML state / far entries keep positions in 29 bits: 3.5 * W * S < 2^29
-    W = std::min<uint64_t>(W, ((uint64_t)1 << 30) / (7ull * P.S));
+    // ML states / far entries keep positions in 29 bits.  A stored position
+    // is below 3p <= 3*W*S (first hit: (c*p - x)/2 with c*p - x < 6p; next
+    // hit after a wave: pos + D*p - W*S with pos < W*S, D <= 3), so
+    // 3*W*S < 2^29 (W <= 170 at S = 2^20: one tile per SM on a B200).
+    W = std::min<uint64_t>(W, (((uint64_t)1 << 29) - 1) / (3ull * P.S));
     W = std::min<uint64_t>(W, P.ntiles);
     P.W = (uint32_t)std::max<uint64_t>(W, 1);
   }
