@@ -443,15 +443,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
     eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 7, d_scal + 8);
     ++launches;
-    uint64_t hb[15];
+    uint64_t hb[16];  // [15] = largest base prime
     CUDA_TRY(cudaMemcpyAsync(hb, d_scal, sizeof(hb), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     const uint64_t nprimes = hb[0];
     if (nprimes > c->max_base_pairs)
       return fail(ERATO_GPU_ALLOC_LIMIT, std::to_string(nprimes) + " base primes exceed cap " +
                                               std::to_string(c->max_base_pairs));
-    uint32_t pmax = 0;
-    if (nprimes) CUDA_TRY(cudaMemcpy(&pmax, c->primes.as<uint32_t>() + nprimes - 1, 4, cudaMemcpyDeviceToHost));
+    const uint32_t pmax = (uint32_t)hb[15];
     // A handful of primes just above the tile size (cfg3: 37) are cheaper as
     // medium primes (a per-tile start offset each) than through the scatter,
     // whose per-wave cost is mostly fixed.

@@ -1372,16 +1372,15 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
       // next hit q + D*p lies d waves ahead (Lemma 2): fp32 estimate of d,
       // then the exact remainder in 32-bit wrap-around arithmetic
       const uint32_t D = wheel_D(s);
+      // (q + D*p < 2^29 + 3*2^32: the fp32 estimate is off by at most one wave)
       uint32_t d = __float2uint_rz(__fmaf_rn((float)D, (float)p, (float)q) * a.inv_ws_f);
       int32_t r = (int32_t)(q + D * p - d * WS);
-      while (r < 0) {
-        r += (int32_t)WS;
-        --d;
-      }
-      while (r >= (int32_t)WS) {
-        r -= (int32_t)WS;
-        ++d;
-      }
+      const bool lo = r < 0;
+      r += lo ? (int32_t)WS : 0;
+      d -= lo ? 1u : 0u;
+      const bool hi = r >= (int32_t)WS;
+      r -= hi ? (int32_t)WS : 0;
+      d += hi ? 1u : 0u;
       const bool keep = ok && d < left;
       uint32_t slot = a.wslot + d;
       if (slot >= ring) slot -= ring;
@@ -1527,12 +1526,15 @@ __global__ void __launch_bounds__(1024) k_write_zeros(const uint32_t* __restrict
   }
 }
 
-// number of entries of a sorted array <= x, for several thresholds
+// number of entries of a sorted array <= x, for several thresholds;
+// out[nthr] = the largest entry (0 if none)
 __global__ void k_bounds(const uint32_t* __restrict__ p, const uint64_t* __restrict__ n_ptr,
                          const uint64_t* __restrict__ thr, int nthr, uint64_t* __restrict__ out) {
   const int i = threadIdx.x;
+  const uint64_t n = *n_ptr;
+  if (i == nthr) out[i] = n ? p[n - 1] : 0;
   if (i >= nthr) return;
-  const uint64_t n = *n_ptr, x = thr[i];
+  const uint64_t x = thr[i];
   uint64_t lo = 0, hi = n;
   while (lo < hi) {
     const uint64_t mid = (lo + hi) >> 1;
