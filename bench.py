@@ -260,12 +260,10 @@ def run_ours(args):
     achieved_gbs = B / (ms / 1e3) / 1e9 / world  # per GPU, each GPU does 1/world of B
     # dominant kernel (largest device time in the phase-timed pass).  Default
     # large-prime path: k_scatter_ml (time in gen_s) + k_scatter_far (bin_s);
-    # ERATO_GPU_SCATTER=fused: one kernel; =genbin: k_gen + k_bin
+    # ERATO_GPU_SCATTER=genbin: k_gen + k_bin
     mode = os.environ.get("ERATO_GPU_SCATTER", "split")
     if mode == "genbin":
         split = {"k_tile": ph.small_s, "k_gen": ph.gen_s, "k_bin": ph.bin_s}
-    elif mode == "fused":
-        split = {"k_tile": ph.small_s, "k_scatter_fused": ph.gen_s + ph.bin_s}
     else:
         split = {"k_tile": ph.small_s, "k_scatter_ml": ph.gen_s, "k_scatter_far": ph.bin_s}
     dom = max(split, key=split.get)
@@ -274,7 +272,6 @@ def run_ours(args):
     alg = {  # algorithmic bytes per launch
         "k_bin": 8.0 * recs / waves,                                   # read + write each record
         "k_gen": (4.0 * recs + 8.0 * ph.base_primes) / waves,          # records out + prime state
-        "k_scatter_fused": (4.0 * recs + 8.0 * ph.base_primes) / waves,  # sorted records out + prime state
         # ML: records out + prime state read/write; far: record out + entry in + entry out
         "k_scatter_ml": (4.0 * (recs - FAR_RECORDS[args.config] / world) + 8.0 * ph.base_primes) / waves,
         "k_scatter_far": 20.0 * FAR_RECORDS[args.config] / world / waves,

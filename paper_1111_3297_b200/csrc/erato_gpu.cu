@@ -306,11 +306,7 @@ void launch_tiles(cudaStream_t st, const eg::TileArgs& a, uint32_t ntiles, bool 
 // Split of the group-per-prime medium primes (indices [0, nwarp) of the
 // medium list, ascending p): counts for 32-lane (p < S/256) and 16-lane
 // (p < S/128) groups, from the list indices of those bounds.
-#ifndef EG_GROUPS
-#define EG_GROUPS 1
-#endif
 void group_split(eg::TileArgs& ta, uint64_t i256, uint64_t i128) {
-  if (!EG_GROUPS) i256 = i128 = ta.nmed_warp;  // 32-lane groups only
   ta.nmed_g32 = (uint32_t)std::min<uint64_t>(i256, ta.nmed_warp);
   ta.nmed_g16 = (uint32_t)std::min<uint64_t>(std::max(i128, i256), ta.nmed_warp) - ta.nmed_g32;
 }

@@ -198,12 +198,6 @@ struct TileArgs {
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
 };
 
-#ifndef EG_HIT_PF
-#define EG_HIT_PF 0
-#endif
-#ifndef EG_RP_PF
-#define EG_RP_PF 1
-#endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 2048;  // medium primes below S/64 (pi(16384) = 1900 at S = 2^20)
 constexpr uint32_t kHitChunk = 256;        // hit records per warp chunk (1 KB of shared staging per warp)
@@ -453,7 +447,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     // p <= S/8, a plain wheel walk for the few-mark primes above
     const uint32_t nlane = a.nmed - a.nmed_warp;
     const uint32_t nitem = (nlane + 31) / 32;
-#if EG_RP_PF
     // the record array is padded (kMedPad): next item's record in flight
     const uint4* rp = a.med + a.nmed_warp + warp * 32 + lane;
     uint4 rec = *rp;
@@ -462,16 +455,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       const bool valid = item * 32 + lane < nlane;
       rp += kTileWarps * 32;
       rec = *rp;
-#else
-    uint32_t item = warp;
-    uint4 rec = make_uint4(0, 0, 0, 0);
-    if (item < nitem && item * 32 + lane < nlane) rec = a.med[a.nmed_warp + item * 32 + lane];
-    for (; item < nitem; item += kTileWarps) {
-      const uint4 cur = rec;
-      const bool valid = item * 32 + lane < nlane;
-      const uint32_t nx = item + kTileWarps;
-      if (nx < nitem && nx * 32 + lane < nlane) rec = a.med[a.nmed_warp + nx * 32 + lane];
-#endif
       if (valid) {
         uint32_t p, s;
         uint32_t q = med_first<P2>(cur, t, tf, x_t, combo_a, p, s);
@@ -1057,10 +1040,9 @@ constexpr uint8_t kNoSlot = 0xff;
 template <int NW, int SL, bool FAR>
 struct ScSmem {
   static constexpr int R = SL * 32;  // staged records per warp
-  static constexpr int RS = R + 32;  // + per-lane trash slots (compacting ML emission)
   static constexpr int FR = FAR ? R : 1;
-  uint32_t reg[NW * RS];   // warp w, step k, lane j at [w*RS + k*32 + j]
-  uint16_t rank[NW * RS];  // rank among this round's records of the same tile
+  uint32_t reg[NW * R];   // warp w, step k, lane j at [w*R + k*32 + j]
+  uint16_t rank[NW * R];  // rank among this round's records of the same tile
   uint32_t srt[NW * R];   // this round's records sorted by tile
   uint64_t freg[NW * FR];
   uint16_t frank[NW * FR];
@@ -1166,7 +1148,7 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
   const uint32_t off_a = smem_addr(sm.off), srt_a = smem_addr(sm.srt), gofs_a = smem_addr(sm.gofs);
   {
     // placement in tile order (sentinels of idle lanes are skipped)
-    const uint32_t rg_a = smem_addr(sm.reg + warp * Sm::RS), rk_a = smem_addr(sm.rank + warp * Sm::RS);
+    const uint32_t rg_a = smem_addr(sm.reg + warp * Sm::R), rk_a = smem_addr(sm.rank + warp * Sm::R);
 #pragma unroll 2
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = lds_u32(rg_a + 4 * i);
@@ -1203,9 +1185,6 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #ifndef EG_ML_STEPS
 #define EG_ML_STEPS 12
 #endif
-#ifndef EG_ML_COMPACT
-#define EG_ML_COMPACT 0
-#endif
 #ifndef EG_FAR_WARPS
 #define EG_FAR_WARPS 8
 #endif
@@ -1235,14 +1214,8 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   const uint32_t B = a.ntiles_w << a.log_s;
   const uint32_t nw = nblk * kMlWarps;
   const uint32_t nu = (a.nml + 31) / 32;
-#if EG_ML_COMPACT
-  const uint32_t lt = (1u << lane) - 1;
-  const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::RS), rank_a = smem_addr(sm.rank + warp * MlSmem::RS);
-  const uint32_t treg_a = reg_a + 4 * (MlSmem::R + lane), trank_a = rank_a + 2 * (MlSmem::R + lane);
-#else
-  const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::RS + lane);
-  const uint32_t rank_a = smem_addr(sm.rank + warp * MlSmem::RS + lane);
-#endif
+  const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::R + lane);
+  const uint32_t rank_a = smem_addr(sm.rank + warp * MlSmem::R + lane);
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
   uint32_t u = blk * kMlWarps + warp;
   uint32_t idx = u * 32 + lane;
@@ -1264,18 +1237,10 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   for (;;) {
     bool rk_pend = false;  // the last staged rank is stored one step late
     uint32_t rk_addr = 0, rk_val = 0;
-#if EG_ML_COMPACT
-    uint32_t k = 0;  // staged records (warp-uniform), compacted with a ballot
-    while (live && k <= (uint32_t)(MlSmem::R - 32)) {
-      const bool v = pos < B;
-      const uint32_t m = __ballot_sync(kFull, v);
-      if (m == 0) {
-#else
     uint32_t k = 0;  // staged steps (warp-uniform)
     while (live && k < (uint32_t)kMlSteps) {
       const bool v = pos < B;
       if (!__any_sync(kFull, v)) {
-#endif
         if (ok) a.ml[idx].y = (pos - WS) | ((s & 7) << 29);
         u += nw;
         if (u >= nu) {
@@ -1293,22 +1258,12 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
         pf[kMlPf - 1] = load(u + kMlPf * nw);
         continue;
       }
-#if EG_ML_COMPACT
-      const uint32_t kk = k + __popc(m & lt);
-      const uint32_t r = stage_rec(v ? cnt_a + ((pos >> shift) << 2) : sink_a, v ? reg_a + (kk << 2) : treg_a, pos);
-      if (rk_pend) st_rank(rk_addr, rk_val);
-      rk_pend = true;
-      rk_addr = v ? rank_a + (kk << 1) : trank_a;
-      rk_val = r;
-      k += __popc(m);
-#else
       const uint32_t r = stage_rec(v ? cnt_a + ((pos >> shift) << 2) : sink_a, reg_a + (k << 7), v ? pos : kNoRec);
       if (rk_pend) st_rank(rk_addr, rk_val);
       rk_pend = true;
       rk_addr = rank_a + (k << 6);
       rk_val = r;
       ++k;
-#endif
       if (v) {
         pos += (dd & 15u) * p;
         dd = rotr4(dd);
@@ -1316,9 +1271,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
       }
     }
     if (rk_pend) st_rank(rk_addr, rk_val);
-#if !EG_ML_COMPACT
     k *= 32;
-#endif
     const int more = __syncthreads_or(live);
     sc_flush(sm, a, k);
     if (!more) break;
@@ -1339,7 +1292,7 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
   const uint32_t nu = (nfar + 31) / 32;
   const uint64_t left = a.nwaves - a.wave;  // waves from this one to the end
   const uint32_t wofs = warp * FarSmem::R + lane;
-  const uint32_t reg_a = smem_addr(sm.reg + warp * FarSmem::RS + lane), rank_a = smem_addr(sm.rank + warp * FarSmem::RS + lane);
+  const uint32_t reg_a = smem_addr(sm.reg + warp * FarSmem::R + lane), rank_a = smem_addr(sm.rank + warp * FarSmem::R + lane);
   const uint32_t ent_a = smem_addr(sm.freg + wofs), slot_a = smem_addr(sm.fslot + wofs),
                  frank_a = smem_addr(sm.frank + wofs);
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
