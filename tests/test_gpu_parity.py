@@ -284,3 +284,38 @@ def test_base_prime_count_fresh_context(restated, l, f, n, overlap):
         if sieve[i]:
             sieve[i * i::i] = False
     assert st.base_primes == int(sieve[3:].sum())
+
+
+def test_medium_record_rebase_over_2p20_tiles(gpu_ctx):
+    """Runs of more than 2^20 tiles re-base the medium-prime records every
+    2^20 tiles (the per-tile fp32 quotient stays exact).  A count-only run of
+    1,049,600 tiles must equal the sum of its two shards, neither of which
+    re-bases."""
+    import paper_1111_3297_b200 as E
+    l, f, n = 30, 1 << 20, 1025  # T = 1025 * 2^30 bits = 1,049,600 tiles of 2^20
+    whole = gpu_ctx.count(E.validate_params(l, f, n))
+    assert whole.tiles > (1 << 20)
+    a = gpu_ctx.count(E.validate_params(l, f, 512))
+    b = gpu_ctx.count(E.validate_params(l, f + 512, n - 512))
+    assert a.tiles < (1 << 20) and b.tiles < (1 << 20)
+    assert whole.prime_count == a.prime_count + b.prime_count
+
+
+@pytest.mark.parametrize("l,f,n", [(21, (1 << 26) - 2048, 300), (22, (1 << 37) - 4096, 400)])
+def test_genbin_fallback_matches_split_scatter(gpu_ctx, l, f, n):
+    """The k_gen + k_bin large-prime path (used when a wave has more than 256
+    bins) gives the same table as the default k_scatter_ml/k_scatter_far path,
+    with ML primes only (first case) and with far buckets (second)."""
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n)
+    ref, sr = gpu_ctx.table(p)
+    old = os.environ.get("ERATO_GPU_SCATTER")
+    os.environ["ERATO_GPU_SCATTER"] = "genbin"
+    try:
+        got, sg = gpu_ctx.table(p)
+    finally:
+        if old is None:
+            del os.environ["ERATO_GPU_SCATTER"]
+        else:
+            os.environ["ERATO_GPU_SCATTER"] = old
+    assert sg.prime_count == sr.prime_count and np.array_equal(got, ref)
