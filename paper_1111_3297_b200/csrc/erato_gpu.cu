@@ -336,6 +336,7 @@ struct Plan {
   unsigned l;
   uint64_t f, n, u, v, T, g0;
   uint32_t log_s, S, W, WS;
+  uint32_t MW;  // ML window: waves walked per ML scatter launch (ML primes: S < p <= MW*WS)
   uint64_t ntiles, nwaves;
   bool overlap;
 };
@@ -385,6 +386,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
   }
   P.WS = P.W * P.S;
   P.nwaves = (P.ntiles + P.W - 1) / P.W;
+  P.MW = 1;  // (an ML walk over 2 waves per launch measured 2 ms slower at cfg5)
 
   uint32_t launches = 0;
   for (int attempt = 0;; ++attempt) {
@@ -433,9 +435,9 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
     }
     // ---------------- 3. class boundaries (one host sync) ----------------
-    // index of the first prime above 61, S/64, S, WS, max(WS/8, S), S/256, S/128
-    uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, P.WS, std::max<uint64_t>(P.WS / 8, P.S), (uint64_t)P.S / 256,
-                       (uint64_t)P.S / 128};
+    // index of the first prime above 61, S/64, S, MW*WS, max(WS/8, S), S/256, S/128
+    uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, (uint64_t)P.MW * P.WS, std::max<uint64_t>(P.WS / 8, P.S),
+                       (uint64_t)P.S / 256, (uint64_t)P.S / 128};
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
     eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 7, d_scal + 8);
     ++launches;
@@ -471,13 +473,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
       CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
-      CUDA_TRY(c->hits.ensure(((uint64_t)P.W * hcap + eg::kScTrash) * 4));  // + trash of the split scatter
-      CUDA_TRY(c->hitcnt.ensure((uint64_t)P.W * 4));
-      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.W * 4, st));
+      // the lists of the MW waves of an ML window, + trash of the split scatter
+      CUDA_TRY(c->hits.ensure(((uint64_t)P.MW * P.W * hcap + eg::kScTrash) * 4));
+      CUDA_TRY(c->hitcnt.ensure((uint64_t)P.MW * P.W * 4));
+      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.MW * P.W * 4, st));
       if (nfar) {
         ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.WS + 3, P.nwaves + 2);
         if (ring > (uint32_t)eg::kMaxRing) return fail(ERATO_GPU_RANGE_TOO_LARGE, "far bucket ring exceeds 256 waves");
-        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.WS))) + 0.01;
+        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.MW * P.WS))) + 0.01;
         const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
         bcap = (uint32_t)std::min<double>((eb * 1.10 + 8192) * c->bcap_scale, (double)nfar + 64);
       }
@@ -582,8 +585,8 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     // k_bin (ERATO_GPU_SCATTER=genbin, or when a wave has more than 256 tiles
     // or ring slots, or 32-bit list offsets do not fit)
     const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
-    const bool sortable = ring <= (uint32_t)eg::kScBins && P.W <= (uint32_t)eg::kScBins;
-    const bool idx32 = (uint64_t)P.W * hcap + eg::kScTrash < (1ull << 32) &&
+    const bool sortable = ring <= (uint32_t)eg::kScBins && (uint64_t)P.MW * P.W <= (uint64_t)eg::kScBins;
+    const bool idx32 = (uint64_t)P.MW * P.W * hcap + eg::kScTrash < (1ull << 32) &&
                        (uint64_t)ring * bcap + eg::kScTrash < (1ull << 32);
     const bool split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
     eg::ScatterArgs sca{};
@@ -638,22 +641,38 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
         ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
+        // this wave's hit lists inside the ML window's lists
+        const uint32_t wi = (uint32_t)(w % P.MW);
+        uint32_t* const hits_w = c->hits.as<uint32_t>() + (uint64_t)wi * P.W * hcap;
+        uint32_t* const hitcnt_w = c->hitcnt.as<uint32_t>() + (uint64_t)wi * P.W;
+        ta.hits = hits_w;
+        ta.hitcnt = hitcnt_w;
         if (split) {
-          sca.wave = w;
-          sca.wslot = slot;
-          sca.ntiles_w = ntw;
-          sca.far_in = ga.far_in;
-          sca.far_in_count = ga.far_in_count;
-          if (nml) {
-            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(sca);
+          if (nml && wi == 0) {  // ML walk over the window's tiles, state re-based by the window span
+            eg::ScatterArgs m = sca;
+            m.ntiles_w = (uint32_t)std::min<uint64_t>((uint64_t)P.MW * P.W, P.ntiles - tile0);
+            m.WS = P.MW * P.WS;
+            m.hits = c->hits.as<uint32_t>();
+            m.hitcnt = c->hitcnt.as<uint32_t>();
+            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(m);
             launches += 1;
           }
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           if (nfar) {
+            sca.wave = w;
+            sca.wslot = slot;
+            sca.ntiles_w = ntw;
+            sca.far_in = ga.far_in;
+            sca.far_in_count = ga.far_in_count;
+            sca.hits = hits_w;
+            sca.hitcnt = hitcnt_w;
             eg::k_scatter_far<<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
             launches += 1;
           }
         } else {
+          // k_gen walks the ML primes wave by wave (any ML bound works)
+          ba.hits = hits_w;
+          ba.hitcnt = hitcnt_w;
           eg::k_gen<<<gen_blocks, eg::kGenThreads, 0, st>>>(ga);
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           eg::k_bin<<<bin_blocks, eg::kBinThreads, sizeof(eg::BinSmem), st>>>(ba);

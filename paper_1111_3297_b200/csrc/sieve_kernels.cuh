@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 // ML primes with p <= WS/8 are walked by 8 lanes (lane j of an octet: wheel
 // class (s+j)&7, step 15p), the others one per lane.
 struct GenArgs {
-  uint2* ml;             // ML primes, ascending: {p, pos | s << 29}
+  uint2* ml;             // ML primes, ascending: {p | s << 29, pos}
   uint32_t nml, noct;    // the first noct ML primes are walked by octets
   const uint64_t* far_in;  // far bucket of this wave
   const uint32_t* far_in_count;
@@ -629,15 +629,15 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     for (; u < uo; u += nw) {
       const uint64_t i = u * 4 + (lane >> 3);
       const bool ok = i < a.noct;
-      const uint32_t p = pn, st = stn;
+      const uint32_t p = pn & 0x1fffffffu, st = stn, cls = pn >> 29;
       const uint64_t inx = (u + nw) * 4 + (lane >> 3);
       if (u + nw < uo && inx < a.noct) {
         const uint2 e = a.ml[inx];
         pn = e.x;
         stn = e.y;
       }
-      const uint32_t s0 = st >> 29;
-      uint32_t pos = ok ? (st & 0x1fffffffu) + p * nib(s_cum[s0], j) : WS;
+      const uint32_t s0 = cls;
+      uint32_t pos = ok ? st + p * nib(s_cum[s0], j) : WS;
       const uint32_t step = 15u * p;
       while (__any_sync(kFull, pos < WS)) {
         const bool v = pos < WS;
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
       m = min(m, __shfl_xor_sync(kFull, m, 2));
       m = min(m, __shfl_xor_sync(kFull, m, 4));
       const uint32_t bal = (__ballot_sync(kFull, ex == m) >> (lane & ~7u)) & 0xffu;
-      if (ok && j == 0) a.ml[i].y = m | (((s0 + __ffs(bal) - 1) & 7) << 29);
+      if (ok && j == 0) a.ml[i] = make_uint2(p | (((s0 + __ffs(bal) - 1) & 7) << 29), m);
     }
   }
   // single ML primes: one per lane (next step's data prefetched)
@@ -667,15 +667,15 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
     for (; u < us; u += nw) {
       const uint64_t i = a.noct + u * 32 + lane;
       const bool ok = i < a.nml;
-      const uint32_t p = pn, st = stn;
+      const uint32_t p = pn & 0x1fffffffu, st = stn, cls = pn >> 29;
       const uint64_t inx = a.noct + (u + nw) * 32 + lane;
       if (u + nw < us && inx < a.nml) {
         const uint2 e = a.ml[inx];
         pn = e.x;
         stn = e.y;
       }
-      uint32_t pos = ok ? (st & 0x1fffffffu) : WS;
-      uint32_t s = st >> 29;
+      uint32_t pos = ok ? st : WS;
+      uint32_t s = cls;
       while (__any_sync(kFull, pos < WS)) {
         const bool v = pos < WS;
         wappend(o, v && pos < lim, pos);
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen(const GenArgs a) {
           s = (s + 1) & 7;
         }
       }
-      if (ok) a.ml[i].y = (pos - WS) | (s << 29);
+      if (ok) a.ml[i] = make_uint2(p | (s << 29), pos - WS);
     }
   }
   // far: exactly one hit in this wave, then re-bucket
@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(kBinThreads) k_bin(const BinArgs a) {
 // Re-bucketed far entries (8 B) go from staging straight to
 // bucket[reserved + rank].
 struct ScatterArgs {
-  uint2* ml;  // ML primes, ascending: {p, pos | s << 29} (pos = next hit from the current wave start)
+  uint2* ml;  // ML primes, ascending: {p | s << 29, pos} (pos = next hit from the current window start)
   uint32_t nml;
   const uint64_t* far_in;  // far bucket of this wave: p | (q | s << 29) << 32
   const uint32_t* far_in_count;
@@ -1033,7 +1033,7 @@ struct ScatterArgs {
   int* overflow;
 };
 
-constexpr int kScBins = 256;            // >= tiles per wave and >= ring slots
+constexpr int kScBins = 256;            // >= tiles per ML window and >= ring slots
 constexpr uint32_t kNoRec = 0xffffffffu;  // staged-slot sentinel (idle lane)
 constexpr uint8_t kNoSlot = 0xff;
 
@@ -1152,7 +1152,7 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #pragma unroll 2
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = lds_u32(rg_a + 4 * i);
-      const uint32_t o = lds_u32(off_a + 4 * ((key >> shift) & (kScBins - 1)));
+      const uint32_t o = lds_u32(off_a + 4 * min(key >> shift, (uint32_t)kScBins - 1));  // sentinels: any bin
       sts_if_rec(srt_a + 4 * (o + lds_u16(rk_a + 2 * i)), key);
     }
   }
@@ -1221,8 +1221,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nml;
   uint2 e0 = ok ? a.ml[idx] : make_uint2(0, 0);
-  uint32_t p = e0.x, y = e0.y;
-  uint32_t pos = ok ? (y & 0x1fffffffu) : B, s = y >> 29;
+  uint32_t p = e0.x & 0x1fffffffu, pos = ok ? e0.y : B, s = e0.x >> 29;
   uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
   // the next kMlPf units' primes and states are in flight (a sparse unit
   // takes only a few steps, far less than a DRAM round trip)
@@ -1241,7 +1240,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
     while (live && k < (uint32_t)kMlSteps) {
       const bool v = pos < B;
       if (!__any_sync(kFull, v)) {
-        if (ok) a.ml[idx].y = (pos - WS) | ((s & 7) << 29);
+        if (ok) a.ml[idx] = make_uint2(p | ((s & 7) << 29), pos - WS);
         u += nw;
         if (u >= nu) {
           live = false;
@@ -1249,9 +1248,9 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
         }
         idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = pf[0].x;
-        pos = ok ? (pf[0].y & 0x1fffffffu) : B;
-        s = pf[0].y >> 29;
+        p = pf[0].x & 0x1fffffffu;
+        pos = ok ? pf[0].y : B;
+        s = pf[0].x >> 29;
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
 #pragma unroll
         for (int k = 0; k + 1 < kMlPf; ++k) pf[k] = pf[k + 1];
@@ -1529,7 +1528,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     // keeps the first hit within 3.5p of the interval start in overlap runs
     const uint64_t pos = first_hit(p, a.x0, 2, s);
     if (i < a.i_ml_end) {
-      a.ml[i - a.i0] = make_uint2(p, (uint32_t)pos | (s << 29));
+      a.ml[i - a.i0] = make_uint2(p | (s << 29), (uint32_t)pos);
     } else {
       // d = pos / WS: fp64 estimate (pos < 2^40, off by at most one), exact fix
       uint64_t d = __double2ull_rz(__dmul_rz(__ull2double_rz(pos), a.inv_ws));
