@@ -1195,7 +1195,10 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #define EG_ML_PF 1
 #endif
 constexpr int kMlWarps = EG_ML_WARPS, kMlSteps = EG_ML_STEPS, kMlPf = EG_ML_PF;
-constexpr int kFarWarps = EG_FAR_WARPS, kFarSteps = EG_FAR_STEPS;
+#ifndef EG_FAR_PF
+#define EG_FAR_PF 2
+#endif
+constexpr int kFarWarps = EG_FAR_WARPS, kFarSteps = EG_FAR_STEPS, kFarPf = EG_FAR_PF;
 using MlSmem = ScSmem<kMlWarps, kMlSteps, false>;
 using FarSmem = ScSmem<kFarWarps, kFarSteps, true>;
 // records / entries one round may send to the trash area
@@ -1302,16 +1305,19 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
     const uint32_t j = uu * 32 + lane;
     return (uu < nu && j < nfar) ? a.far_in[j] : 0;
   };
-  uint64_t ne0 = load(u), ne1 = load(u + nw);
+  uint64_t pfe[kFarPf];  // entries of the next kFarPf units in flight
+#pragma unroll
+  for (int j = 0; j < kFarPf; ++j) pfe[j] = load(u + j * nw);
   uint32_t rk1 = 0, rk2 = 0;  // ranks of the last step, stored one step late
   for (;;) {
     uint32_t k = 0;  // staged steps (warp-uniform)
     for (; u < nu && k < (uint32_t)kFarSteps; ++k) {
       const uint32_t i = u * 32 + lane;
       const bool ok = i < nfar;
-      const uint64_t e = ne0;
-      ne0 = ne1;
-      ne1 = load(u + 2 * nw);
+      const uint64_t e = pfe[0];
+#pragma unroll
+      for (int j = 0; j + 1 < kFarPf; ++j) pfe[j] = pfe[j + 1];
+      pfe[kFarPf - 1] = load(u + kFarPf * nw);
       u += nw;
       const uint32_t p = (uint32_t)e, q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
       const bool emit = ok && q < lim;
