@@ -62,7 +62,7 @@ LARGE_RECORDS = {1: 0, 2: 0, 3: 0, 4: 835_065_655, 5: 7_429_219_143}
 FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_802_335_964}
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # (profiles/r01_ncu_summary.txt, cfg5 wave 100)
-NCU_TRAFFIC = {5: {"k_tile": 134.0e6 + 3.7e6, "k_scatter_ml": 68.5e6 + 110.6e6, "k_scatter_far": 64.4e6 + 42.7e6}}
+NCU_TRAFFIC = {5: {"k_tile": 135.7e6 + 5.6e6, "k_scatter_ml": 69.5e6 + 113.1e6, "k_scatter_far": 64.9e6 + 42.6e6}}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 R_ATOM_MEASURED = 3.47e12  # smem atomicOr/s per B200, microbench/mb_atomics.cu (profiles/r01_microbench_atomics.log)
 
