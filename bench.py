@@ -58,8 +58,11 @@ ROOF = {
 # tiles), tools/roofline_counts.py `ours_large_records`: k_bin moves 8 B per record.
 # (cfg3's 37 primes just above the tile size are sieved as medium primes: no records)
 LARGE_RECORDS = {1: 0, 2: 0, 3: 0, 4: 835_065_655, 5: 7_429_219_143}
-# ... of which come from far primes (p > WS = 146 tiles), `ours_far_records`
-FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_802_335_964}
+# ... of which come from far primes (p > WS = 148 tiles), `ours_far_records`
+FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_789_110_090}
+# Medium-prime marks (smem atomics in k_tile) of this implementation, `ours_medium_marks`
+# (cfg3: + its 37 primes just above the tile size, sieved as medium primes)
+MEDIUM_MARKS = {1: 2_704_493, 2: 2_151_023_657, 3: 673_995_484, 4: 5_391_802_774, 5: 21_567_210_790}
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # (profiles/r01_ncu_summary.txt, cfg5 wave 100)
 NCU_TRAFFIC = {5: {"k_tile": 135.7e6 + 5.6e6, "k_scatter_ml": 69.5e6 + 113.1e6, "k_scatter_far": 64.9e6 + 42.6e6}}
@@ -279,6 +282,12 @@ def run_ours(args):
     }
     launch_s = split[dom] / waves
     dom_gbs = alg[dom] / launch_s / 1e9 if launch_s > 0 else 0.0
+    # the tile kernel's other bound: its shared-memory atomics (medium marks + hit records)
+    tile_launch_s = split["k_tile"] / waves
+    tile_atoms = (MEDIUM_MARKS[args.config] + LARGE_RECORDS[args.config]) / world / waves
+    tile_atomic = {"kernel": "k_tile", "achieved": round(tile_atoms / tile_launch_s, 1) if tile_launch_s > 0 else 0.0,
+                   "peak": R_ATOM_MEASURED, "unit": "smem atomics/s",
+                   "frac": round(tile_atoms / tile_launch_s / R_ATOM_MEASURED, 4) if tile_launch_s > 0 else 0.0}
     roof = {
         "bound": "hbm",
         "kernel": dom,
@@ -290,6 +299,7 @@ def run_ours(args):
         "alg_bytes_per_launch": alg[dom],
         "launch_us": round(launch_s * 1e6, 2),
         "peak_source": hbm_src,
+        "tile_atomic": tile_atomic,
     }
     run_roof = {
         "bound": bound,

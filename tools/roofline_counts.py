@@ -45,7 +45,7 @@ def odd_upto(x: np.ndarray) -> np.ndarray:
     return (np.maximum(x, 0) + 1) // 2
 
 
-def counts(l: int, f: int, n: int, log_tile: int = 20, wave_tiles: int = 146):
+def counts(l: int, f: int, n: int, log_tile: int = 20, wave_tiles: int = 148):
     R = Restated()
     u = (f << (l + 1)) + 1
     v = (f + n) << (l + 1)
