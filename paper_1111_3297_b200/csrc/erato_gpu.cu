@@ -3,16 +3,16 @@
 // Replaces run_sieve (/root/reference/proj/src/driver.cpp:83-120) and its
 // sinks.  Per run:
 //   init  (base.cpp:19-89 analog, all on the device)
-//     1. odd primes < 2^16 (cached per context), Barrett constants
+//     1. odd primes < 2^16 and pattern tables (cached per context)
 //     2. sieve [1, isqrt(v)] with the tile kernel -> bitmap -> sorted u32
 //        prime list (popcount + scan compaction)
-//     3. one host sync: prime count and the class boundaries
-//     4. large primes: first hits (64-bit, __umul64hi) -> ML array + far
-//        wave buckets
+//     3. one host sync: prime count, class boundaries, largest prime
+//     4. large primes: first hits (fp64 quotient estimate + exact u64
+//        remainder) -> ML array + far wave buckets
 //   waves (the reference's per-segment loop, driver.cpp:93-117)
-//     for each wave of W tiles: scatter (large primes -> per-tile hit
-//     records, re-bucket) then tile kernel (patterns, medium, hits,
-//     popcount, 128-bit write-out)
+//     for each wave of W tiles: k_scatter_ml + k_scatter_far (large primes
+//     -> per-tile hit records, far entries re-bucketed) then k_tile
+//     (patterns, medium primes, hits, popcount, 128-bit write-out)
 //   count: device u64 (NullSink: only it leaves the device).
 #include <cuda_runtime.h>
 #include <fcntl.h>

@@ -12,13 +12,15 @@
 //   small   p <= 61        periodic word patterns (masks.cpp:9-50 idea)
 //   medium  61 < p <= S    shared-memory atomicOr marking inside the tile,
 //                          start offset recomputed per tile from 32-bit
-//                          residues (MedRecs), mod-30 wheel over the cofactor
-//                          (wheel.cpp:10-69 idea: 8 of 15 odd cofactors)
-//   large   p > S          bucketed: (p,q) entries scattered into the wave
-//                          of their next hit, which emits per-tile hit
-//                          records; the paper's circle/bucket idea
-//                          (large_kernel.hpp, Lemma 2) rebuilt for
-//                          a machine that processes ~148 tiles at once.
+//                          residues (k_med_records), mod-30 wheel over the
+//                          cofactor (wheel.cpp:10-69 idea: 8 of 15 odd
+//                          cofactors)
+//   ML      S < p <= W*S   walked once per wave (k_scatter_ml) into per-tile
+//                          hit records
+//   far     p > W*S        (p,q) entries in the bucket of the wave of their
+//                          next hit (k_scatter_far): the paper's circle /
+//                          bucket idea (large_kernel.hpp, Lemma 2)
+//                          rebuilt for a machine that sieves 148 tiles at once
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -1300,7 +1302,7 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
   const uint32_t fcnt_a = smem_addr(sm.fcnt), fsink_a = fcnt_a + 4 * (kScBins + lane);
   uint32_t u = blk * kFarWarps + warp;
-  // the entries of the next two units are in flight (loads issued early)
+  // the entries of the next kFarPf units are in flight (loads issued early)
   auto load = [&](uint32_t uu) -> uint64_t {
     const uint32_t j = uu * 32 + lane;
     return (uu < nu && j < nfar) ? a.far_in[j] : 0;
