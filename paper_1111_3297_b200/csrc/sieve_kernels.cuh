@@ -297,6 +297,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   }
   __syncthreads();
 
+  const uint64_t x_t = 2 * g + 1;
+  const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^20)
+  const float tf = __uint2float_rz(t);
+  const uint32_t combo_a = smem_addr(s_combo);
+  // 0. start offsets of the group-marked medium primes (p < S/64), lane-
+  // parallel into shared memory (no barrier of its own: phase 1's covers it)
+  for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
+    uint32_t p, s;
+    const uint32_t q0 = med_first<P2>(a.med[i], t, tf, x_t, combo_a, p, s);
+    s_wq[i] = make_uint2(q0, p | (s << 29));
+  }
+
   // 1. small primes: OR of the 8 group windows.  Lane l of a warp builds
   // words l, l+32, l+64, l+96 of the warp's 128-word block: one phase
   // update per 4 words, conflict-free loads (each group table is padded by
@@ -341,21 +353,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 
   // 2. medium primes
   {
-    const uint64_t x_t = 2 * g + 1;
-    const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^20)
-    const float tf = __uint2float_rz(t);
-    const uint32_t combo_a = smem_addr(s_combo);
-    // 2a. group-per-prime (p < S/64): start offsets computed lane-parallel
-    // into shared memory; then a group of G lanes takes one prime, lane j
+    // 2a. group-per-prime (p < S/64): start offsets were computed
+    // lane-parallel into shared memory (above); a group of G lanes takes one prime, lane j
     // marking wheel class (s+j)&7 of period j>>3 (step G/8 wheel periods):
     // G = 32 for p < S/256, 16 below S/128, 8 below S/64 — every lane makes
     // at least ~4 marks.
-    for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
-      uint32_t p, s;
-      const uint32_t q0 = med_first<P2>(a.med[i], t, tf, x_t, combo_a, p, s);
-      s_wq[i] = make_uint2(q0, p | (s << 29));
-    }
-    __syncthreads();
     const uint32_t n32 = a.nmed_g32, n16 = a.nmed_g16, i16 = (n16 + 1) >> 1;
     const uint32_t nitems = n32 + i16 + (a.nmed_warp - n32 - n16 + 3) / 4;
     // 3. large primes: this tile's hit records, in chunks of kHitChunk per
