@@ -45,12 +45,21 @@ enum {
   ERATO_GPU_E_CUDA = 64,
   ERATO_GPU_E_NO_DEVICE = 65,
   ERATO_GPU_E_INVALID_ARG = 66,
+  ERATO_GPU_E_INVARIANT = 67, /* ERATO_GPU_CHECK_INVARIANTS found a large-prime bookkeeping error */
 };
 
 /* flags */
 #define ERATO_GPU_TEST_MODE 0x1u     /* l >= 4 instead of 10 (params.hpp:58-60) */
 #define ERATO_GPU_ALLOW_OVERLAP 0x2u /* accept u^2 <= v incl. f = 0 (SURVEY §8c convention:
                                         multiples from max(u, p^2); 1 and primes stay 0) */
+#define ERATO_GPU_CHECK_INVARIANTS 0x200u /* device checks of the large-prime path (the analog of
+                                             validate_circle_invariants, src/kernels.cpp:103-179,
+                                             and acceptance.cpp:122-161 "each multiple exactly
+                                             once"): every far entry read from a wave's bucket hits
+                                             inside that wave, and the hit records consumed by the
+                                             tiles equal the admissible multiples of the large
+                                             primes in the tiles (counted per prime in closed
+                                             form); a violation fails with ERATO_GPU_E_INVARIANT */
 #define ERATO_GPU_PHASE_TIMING 0x100u /* CUDA events around every launch: fills small_s (tile
                                          kernel) and large_s (bucket scatter) in the stats */
 
@@ -71,9 +80,9 @@ typedef struct {
   uint32_t waves;
   uint32_t kernel_launches;
   uint32_t retries; /* capacity re-runs after a bucket overflow */
-  double gen_s;     /* with ERATO_GPU_PHASE_TIMING: k_gen (large-prime walk) */
-  double bin_s;     /* with ERATO_GPU_PHASE_TIMING: k_bin (hit-record sort) */
-  uint64_t large_records; /* hit records of large primes (written by k_gen) */
+  double gen_s;     /* with ERATO_GPU_PHASE_TIMING: ML scatter (k_scatter_ml; k_gen on the fallback) */
+  double bin_s;     /* with ERATO_GPU_PHASE_TIMING: far scatter (k_scatter_far; k_bin on the fallback) */
+  uint64_t large_records; /* with ERATO_GPU_CHECK_INVARIANTS: hit records consumed by the tiles */
 } erato_gpu_stats;
 
 /* ---- host-side parameter logic (no device needed) ---------------------- */

@@ -123,6 +123,7 @@ const char* erato_gpu_errc_name(int code) {
     case ERATO_GPU_E_CUDA: return "CUDA_ERROR";
     case ERATO_GPU_E_NO_DEVICE: return "NO_DEVICE";
     case ERATO_GPU_E_INVALID_ARG: return "INVALID_ARGUMENT";
+    case ERATO_GPU_E_INVARIANT: return "INVARIANT";
   }
   return "UNKNOWN";
 }
@@ -396,7 +397,11 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
     uint64_t nbase_bits = (vroot + 1) / 2;  // odd numbers 1..vroot
     const uint64_t prime_cap = pi_upper(vroot) + 64;
     CUDA_TRY(c->primes.ensure(prime_cap * 4));
-    uint64_t* d_scal = c->scal.as<uint64_t>();  // [0] total primes, [8..] bounds, [16] count, [17] overflow
+    // [0] total primes, [8..15] bounds + largest prime, [16] count, [17] overflow,
+    // [18] hit records consumed, [19] expected records, [20] base-sieve count, [21] bad far entry
+    uint64_t* d_scal = c->scal.as<uint64_t>();
+    CUDA_TRY(cudaMemsetAsync(d_scal + 18, 0, 16, st));
+    CUDA_TRY(cudaMemsetAsync(d_scal + 21, 0, 8, st));
     if (nbase_bits > 1) {
       const uint64_t words = ((nbase_bits + ((1u << kBaseLogTile) - 1)) >> kBaseLogTile) << (kBaseLogTile - 5);
       CUDA_TRY(c->base_bits.ensure(words * 4));
@@ -515,9 +520,18 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       sa.WS = P.WS;
       sa.inv_ws = 1.0 / (double)P.WS;
       sa.overflow = reinterpret_cast<int*>(d_scal + 17);
+      if (const char* inj = std::getenv("ERATO_GPU_TEST_INJECT")) sa.inject = std::atoi(inj);  // tests only
       const uint64_t nl = nprimes - iS;
       eg::k_setup_large<<<(unsigned)((nl + eg::kSetupThreads - 1) / eg::kSetupThreads), eg::kSetupThreads, 0, st>>>(sa);
       ++launches;
+      if (flags & ERATO_GPU_CHECK_INVARIANTS) {
+        // expected hit records: admissible multiples of the large primes in the tiles
+        const unsigned __int128 x_hi = (unsigned __int128)P.u + 2 * (unsigned __int128)(P.ntiles << P.log_s) - 2;
+        const uint64_t xh = x_hi > UINT64_MAX ? UINT64_MAX : (uint64_t)x_hi;
+        eg::k_expected_records<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(
+            c->primes.as<uint32_t>(), iS, nprimes, P.u, xh, reinterpret_cast<unsigned long long*>(d_scal + 19));
+        ++launches;
+      }
     } else {
       CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));
     }
@@ -684,6 +698,12 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
           evi += 3;
         }
         ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
+        if (flags & ERATO_GPU_CHECK_INVARIANTS) {
+          eg::k_check_wave<<<(unsigned)c->nsm, 256, 0, st>>>(
+              hitcnt_w, ntw, hcap, nfar ? ga.far_in : nullptr, ga.far_in_count, bcap, P.WS,
+              reinterpret_cast<unsigned long long*>(d_scal + 18), reinterpret_cast<int*>(d_scal + 21));
+          ++launches;
+        }
       }
       ta.tile0 = tile0;
       if (tile0 + ntw - ta.tbase > eg::kMaxChunkTiles && nmed) {
@@ -718,8 +738,8 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       }
       return 0;  // overflow cannot be checked without a sync; capacities are generous
     }
-    uint64_t res[2];
-    CUDA_TRY(cudaMemcpyAsync(res, d_scal + 16, 16, cudaMemcpyDeviceToHost, st));
+    uint64_t res[6];  // d_scal[16..21]
+    CUDA_TRY(cudaMemcpyAsync(res, d_scal + 16, sizeof(res), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     if ((int)res[1] != 0) {
       if (attempt >= 4) return fail(ERATO_GPU_ALLOC_LIMIT, "bucket capacity overflow persists");
@@ -727,6 +747,13 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       c->bcap_scale *= 2.0;
       if (stats) stats->retries = attempt + 1;
       continue;
+    }
+    if ((flags & ERATO_GPU_CHECK_INVARIANTS) && have_large) {
+      if (res[5])
+        return fail(ERATO_GPU_E_INVARIANT, "a far bucket entry does not hit inside the wave of its bucket");
+      if (res[2] != res[3])
+        return fail(ERATO_GPU_E_INVARIANT, "large-prime hit records " + std::to_string(res[2]) + " != " +
+                                               std::to_string(res[3]) + " admissible multiples in the tiles");
     }
     if (stats) {
       float t_init = 0, t_tot = 0;
@@ -736,6 +763,7 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       std::memset(stats, 0, sizeof(*stats));
       stats->retries = retries;
       stats->prime_count = res[0];
+      stats->large_records = res[2];  // (counted with ERATO_GPU_CHECK_INVARIANTS)
       stats->segments = n;
       stats->init_s = t_init * 1e-3;
       stats->small_s = (t_tot - t_init) * 1e-3;

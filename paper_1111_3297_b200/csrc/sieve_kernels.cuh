@@ -1519,6 +1519,7 @@ struct SetupArgs {
   uint32_t WS;
   double inv_ws;
   int* overflow;
+  int inject;  // test-only fault injection on the first far prime: 1 drop its entry, 2 corrupt its q
 };
 
 constexpr int kSetupThreads = 1024;
@@ -1548,6 +1549,10 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
         app = true;
         slotb = (uint32_t)d % a.ring;
         ne = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
+        if (a.inject && i == a.i_ml_end) {
+          if (a.inject == 1) app = false;
+          else ne |= (uint64_t)0x1fffffffu << 32;  // q beyond the wave
+        }
       }
     }
   }
@@ -1567,6 +1572,53 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     if (pos < a.bcap) a.far_buckets[(uint64_t)slotb * a.bcap + pos] = ne;
     else atomicExch(a.overflow, 1);
   }
+}
+
+// ---- invariant checks (ERATO_GPU_CHECK_INVARIANTS), separate launches so
+// the wave kernels are untouched.  Per wave, between the scatter and the
+// tiles: sum the hit records the tiles are about to consume, and check that
+// every far entry of the wave's bucket hits inside the wave.
+__global__ void __launch_bounds__(256) k_check_wave(const uint32_t* __restrict__ hitcnt, uint32_t ntiles_w,
+                                                    uint32_t hcap, const uint64_t* __restrict__ far_in,
+                                                    const uint32_t* __restrict__ far_in_count, uint32_t bcap,
+                                                    uint32_t WS, unsigned long long* rec_count, int* bad) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ntiles_w) atomicAdd(rec_count, (unsigned long long)min(hitcnt[i], hcap));
+  if (far_in) {
+    const uint32_t nfar = min(*far_in_count, bcap);
+    for (uint32_t j = i; j < nfar; j += gridDim.x * blockDim.x)
+      if (((uint32_t)(far_in[j] >> 32) & 0x1fffffffu) >= WS) atomicExch(bad, 1);
+  }
+}
+
+// ---- invariant check: admissible multiples of the large primes in the tiles
+// (ERATO_GPU_CHECK_INVARIANTS).  For prime p the hit records are the
+// multiples c*p, c coprime to 30 and c >= 2, of odd numbers in [x_lo, x_hi]
+// (the run's tiles; the first hit uses cofactor >= 2, k_setup_large).
+__device__ __forceinline__ uint64_t coprime30_upto(uint64_t n) {  // #{1 <= c <= n : gcd(c, 30) = 1}
+  constexpr uint8_t cnt[30] = {0, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 4, 4, 4, 4, 5, 5, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 8};
+  return 8 * (n / 30) + cnt[n % 30];
+}
+__device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {  // fp64 estimate + exact fix
+  uint64_t q = __double2ull_rz(__dmul_rz(__ull2double_rz(x), __drcp_rn((double)p)));
+  if (q * p > x) --q;
+  if ((q + 1) * p <= x) ++q;
+  return q;
+}
+__global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __restrict__ primes, uint64_t i0,
+                                                          uint64_t i1, uint64_t x_lo, uint64_t x_hi,
+                                                          unsigned long long* __restrict__ out) {
+  const uint64_t i = i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long cnt = 0;
+  if (i < i1) {
+    const uint32_t p = primes[i];
+    uint64_t c_lo = div_floor(x_lo - 1, p) + 1;  // ceil(x_lo / p)
+    if (c_lo < 2) c_lo = 2;
+    const uint64_t c_hi = div_floor(x_hi, p);
+    if (c_hi >= c_lo) cnt = coprime30_upto(c_hi) - coprime30_upto(c_lo - 1);
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
 }
 
 }  // namespace eg

@@ -34,6 +34,7 @@ from . import _lib
 
 TEST_MODE = 0x1
 ALLOW_OVERLAP = 0x2
+CHECK_INVARIANTS = 0x200  # device checks of the large-prime bookkeeping (erato_gpu.h)
 
 kMinLogSeg = 10
 kMinLogSegTest = 4
@@ -57,6 +58,7 @@ class errc(enum.IntEnum):
     cuda_error = 63
     no_device = 64
     invalid_argument = 65
+    invariant = 66
 
 
 _ERRC_NAMES = {
@@ -66,6 +68,7 @@ _ERRC_NAMES = {
     errc.alloc_limit: "ALLOC_LIMIT", errc.limit_too_large: "LIMIT_TOO_LARGE",
     errc.range_too_large: "RANGE_TOO_LARGE", errc.io_error: "IO_ERROR",
     errc.cuda_error: "CUDA_ERROR", errc.no_device: "NO_DEVICE", errc.invalid_argument: "INVALID_ARGUMENT",
+    errc.invariant: "INVARIANT",
 }
 
 PARAM_ERRORS = (errc.l_out_of_range, errc.f_zero_or_overlap, errc.n_out_of_range, errc.overflow,
@@ -255,10 +258,13 @@ class Context:
         _check(_lib.load().erato_gpu_set_max_base_pairs(self._h, n))
 
     # ---- raw calls ------------------------------------------------------
-    def count(self, params: SieveParams) -> RunStats:
+    def count(self, params: SieveParams, check_invariants: bool = False) -> RunStats:
+        """NullSink run; check_invariants adds the device checks of the
+        large-prime path (validate_circle_invariants analog)."""
         st = _lib.Stats()
         cnt = C.c_uint64()
-        _check(_lib.load().erato_gpu_count(self._h, params.l, params.f, params.n, params.flags,
+        flags = params.flags | (CHECK_INVARIANTS if check_invariants else 0)
+        _check(_lib.load().erato_gpu_count(self._h, params.l, params.f, params.n, flags,
                                            C.byref(cnt), C.byref(st)))
         return RunStats._from(st)
 

@@ -319,3 +319,42 @@ def test_genbin_fallback_matches_split_scatter(gpu_ctx, l, f, n):
         else:
             os.environ["ERATO_GPU_SCATTER"] = old
     assert sg.prime_count == sr.prime_count and np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("l,f,n,mode", [(21, (1 << 26) - 2048, 512, None), (22, (1 << 37) - 4096, 256, None),
+                                         (22, (1 << 37) - 4096, 256, "genbin"), (20, 1 << 21, 40, None)])
+def test_large_prime_invariants_hold(gpu_ctx, l, f, n, mode):
+    """ERATO_GPU_CHECK_INVARIANTS (validate_circle_invariants analog,
+    src/kernels.cpp:103-179; acceptance.cpp:122-161 'each multiple exactly
+    once'): far entries hit inside their bucket's wave, and the records the
+    tiles consume equal the admissible multiples of the large primes."""
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n)
+    old = os.environ.get("ERATO_GPU_SCATTER")
+    if mode:
+        os.environ["ERATO_GPU_SCATTER"] = mode
+    try:
+        st = gpu_ctx.count(p, check_invariants=True)
+    finally:
+        if mode:
+            if old is None:
+                del os.environ["ERATO_GPU_SCATTER"]
+            else:
+                os.environ["ERATO_GPU_SCATTER"] = old
+    assert st.large_records > 0
+    assert st.prime_count == gpu_ctx.count(p).prime_count
+
+
+@pytest.mark.parametrize("inject,what", [("1", "admissible multiples"), ("2", "does not hit inside")])
+def test_large_prime_invariants_catch_injected_faults(gpu_ctx, inject, what):
+    """Fault injection (test_kernels.cpp:391-404 idea): dropping one far entry
+    or corrupting its q must be reported as INVARIANT."""
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(22, (1 << 37) - 4096, 256)
+    os.environ["ERATO_GPU_TEST_INJECT"] = inject
+    try:
+        with pytest.raises(E.Error) as ei:
+            gpu_ctx.count(p, check_invariants=True)
+    finally:
+        del os.environ["ERATO_GPU_TEST_INJECT"]
+    assert ei.value.code == E.errc.invariant and what in str(ei.value)
