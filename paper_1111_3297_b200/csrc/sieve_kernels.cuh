@@ -1363,7 +1363,10 @@ __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs 
   extern __shared__ uint4 smem_raw[];
   scatter_ml(a, blockIdx.x, gridDim.x, *reinterpret_cast<MlSmem*>(smem_raw));
 }
-__global__ void __launch_bounds__(kFarWarps * 32) k_scatter_far(const ScatterArgs a) {
+#ifndef EG_FAR_MINB
+#define EG_FAR_MINB 1
+#endif
+__global__ void __launch_bounds__(kFarWarps * 32, EG_FAR_MINB) k_scatter_far(const ScatterArgs a) {
   extern __shared__ uint4 smem_raw[];
   scatter_far(a, blockIdx.x, gridDim.x, *reinterpret_cast<FarSmem*>(smem_raw));
 }
