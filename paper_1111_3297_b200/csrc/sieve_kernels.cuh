@@ -1359,7 +1359,14 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
   }
 }
 
+#ifndef EG_ML_MINB
+#define EG_ML_MINB 0
+#endif
+#if EG_ML_MINB
+__global__ void __launch_bounds__(kMlWarps * 32, EG_ML_MINB) k_scatter_ml(const ScatterArgs a) {
+#else
 __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs a) {
+#endif
   extern __shared__ uint4 smem_raw[];
   scatter_ml(a, blockIdx.x, gridDim.x, *reinterpret_cast<MlSmem*>(smem_raw));
 }
