@@ -93,6 +93,8 @@ struct erato_gpu_ctx {
   int device = 0;
   int nsm = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t xstream = nullptr;               // D2H copies of finished waves (sieve_to_host)
+  cudaEvent_t xev = nullptr, xjoin = nullptr;   // wave done / copies done
   // cached per context
   DevBuf sp, spm, ptab;  // small primes < 2^16, their base-sieve records, pattern tables
   std::vector<uint32_t> h_sp;
@@ -240,6 +242,9 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   c->nsm = prop.multiProcessorCount;
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->xjoin, cudaEventDisableTiming));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   for (auto kt : {eg::k_tile<false, false>, eg::k_tile<true, false>, eg::k_tile<false, true>, eg::k_tile<true, true>})
     CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -282,6 +287,9 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->phase_ev) cudaEventDestroy(e);
+  if (c->xev) cudaEventDestroy(c->xev);
+  if (c->xjoin) cudaEventDestroy(c->xjoin);
+  if (c->xstream) cudaStreamDestroy(c->xstream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -344,9 +352,11 @@ struct Plan {
 
 }  // namespace
 
-extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
-                             void* dev_table, uint64_t* dev_count, void* stream_v, int sync,
-                             erato_gpu_stats* stats) {
+namespace {
+// host_dst (pinned, optional): each wave's finished slice of dev_table is
+// copied to host_dst on a side stream while the next waves run.
+int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags, void* dev_table,
+             uint64_t* dev_count, void* stream_v, int sync, erato_gpu_stats* stats, uint8_t* host_dst) {
   if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
   Plan P{};
   int rc = erato_gpu_validate(l, f, n, flags, &P.u, &P.v);
@@ -716,12 +726,23 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
       }
       if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
       launch_tiles(st, ta, ntw, P.overlap);
+      if (host_dst && dev_table) {  // output pipeline: this wave's bytes go to the host now
+        const uint64_t b0 = (tile0 << P.log_s) / 8, b1 = std::min<uint64_t>((tile0 + ntw) << P.log_s, P.T) / 8;
+        CUDA_TRY(cudaEventRecord(c->xev, st));
+        CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->xev, 0));
+        CUDA_TRY(cudaMemcpyAsync(host_dst + b0, static_cast<uint8_t*>(dev_table) + b0, b1 - b0,
+                                 cudaMemcpyDeviceToHost, c->xstream));
+      }
       if (timing) {
         CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
         ev_pairs.push_back({evi, false});
         evi += 2;
       }
       ++launches;
+    }
+    if (host_dst && dev_table) {  // join the copies
+      CUDA_TRY(cudaEventRecord(c->xjoin, c->xstream));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->xjoin, 0));
     }
     CUDA_TRY(cudaGetLastError());
     if (dev_count) CUDA_TRY(cudaMemcpyAsync(dev_count, d_count, 8, cudaMemcpyDeviceToDevice, st));
@@ -797,6 +818,14 @@ extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t 
   }
 }
 
+}  // namespace
+
+extern "C" int erato_gpu_run(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                             void* dev_table, uint64_t* dev_count, void* stream_v, int sync,
+                             erato_gpu_stats* stats) {
+  return run_impl(c, l, f, n, flags, dev_table, dev_count, stream_v, sync, stats, nullptr);
+}
+
 extern "C" int erato_gpu_count(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
                                uint64_t* count, erato_gpu_stats* stats) {
   erato_gpu_stats local{};
@@ -820,8 +849,13 @@ extern "C" int erato_gpu_sieve_to_host(erato_gpu_ctx* c, unsigned l, uint64_t f,
   erato_gpu_stats local{};
   erato_gpu_stats* s = stats ? stats : &local;
   std::memset(s, 0, sizeof(*s));
-  rc = erato_gpu_run(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, s);
+  // pinned destination: copy each wave's slice while the next waves run
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  rc = run_impl(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, s, pinned ? dst : nullptr);
   if (rc) return rc;
+  if (pinned) return 0;  // (output_s stays 0: the copies overlapped the sieve)
   CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
   CUDA_TRY(cudaMemcpyAsync(dst, c->table.p, bytes, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));

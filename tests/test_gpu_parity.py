@@ -358,3 +358,17 @@ def test_large_prime_invariants_catch_injected_faults(gpu_ctx, inject, what):
     finally:
         del os.environ["ERATO_GPU_TEST_INJECT"]
     assert ei.value.code == E.errc.invariant and what in str(ei.value)
+
+
+@pytest.mark.parametrize("l,f,n", [(22, (1 << 37) - 4096, 300), (20, 523776, 333)])
+def test_pinned_output_pipeline_matches(gpu_ctx, l, f, n):
+    """sieve_to_host into pinned memory copies each wave's slice while the
+    next waves run (output pipeline); the bytes equal the
+    pageable path's single copy."""
+    import torch
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n)
+    ref, sr = gpu_ctx.table(p)
+    pinned = torch.empty(p.table_bytes(), dtype=torch.uint8, pin_memory=True)
+    got, sg = gpu_ctx.table(p, out=pinned.numpy())
+    assert sg.prime_count == sr.prime_count and np.array_equal(got, ref)
