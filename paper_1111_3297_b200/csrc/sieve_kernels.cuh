@@ -1609,10 +1609,13 @@ __device__ __forceinline__ uint64_t coprime30_upto(uint64_t n) {  // #{1 <= c <=
   constexpr uint8_t cnt[30] = {0, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 4, 4, 4, 4, 5, 5, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 8};
   return 8 * (n / 30) + cnt[n % 30];
 }
-__device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {  // fp64 estimate + exact fix
+__device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {
+  // fp64 estimate (off by at most one), exact fix on the remainder in
+  // wrap-around u64 arithmetic (q*p may pass 2^64 when x is near it)
   uint64_t q = __double2ull_rz(__dmul_rz(__ull2double_rz(x), __drcp_rn((double)p)));
-  if (q * p > x) --q;
-  if ((q + 1) * p <= x) ++q;
+  int64_t r = (int64_t)(x - q * p);
+  if (r < 0) --q;
+  else if (r >= (int64_t)p) ++q;
   return q;
 }
 __global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __restrict__ primes, uint64_t i0,

@@ -372,3 +372,25 @@ def test_pinned_output_pipeline_matches(gpu_ctx, l, f, n):
     pinned = torch.empty(p.table_bytes(), dtype=torch.uint8, pin_memory=True)
     got, sg = gpu_ctx.table(p, out=pinned.numpy())
     assert sg.prime_count == sr.prime_count and np.array_equal(got, ref)
+
+
+def test_near_2p64_far_path_exact(gpu_ctx):
+    """v just below 2^64 with the base-prime cap raised: base primes up to
+    2^32 (far entries with D*p past 2^32, fp64 first hits near 2^64).  The
+    large-prime invariants hold and 600 Miller-Rabin samples of the table
+    agree bit for bit."""
+    import paper_1111_3297_b200 as E
+    l = 30
+    f = (((1 << 64) - 1) >> (l + 1)) - 1
+    p = E.validate_params(l, f, 1)
+    gpu_ctx.set_max_base_pairs(1 << 28)
+    try:
+        st = gpu_ctx.count(p, check_invariants=True)
+        g, st2 = gpu_ctx.table(p)
+    finally:
+        gpu_ctx.set_max_base_pairs(1 << 27)
+    assert st.prime_count == st2.prime_count and st.large_records > 0
+    rng = np.random.default_rng(7)
+    for j in rng.integers(0, p.table_bits(), 600):
+        j = int(j)
+        assert ((int(g[j >> 3]) >> (j & 7)) & 1) == (0 if miller_rabin(p.u + 2 * j) else 1)
