@@ -389,8 +389,40 @@ def test_near_2p64_far_path_exact(gpu_ctx):
         g, st2 = gpu_ctx.table(p)
     finally:
         gpu_ctx.set_max_base_pairs(1 << 27)
+    assert ran >= 10
     assert st.prime_count == st2.prime_count and st.large_records > 0
     rng = np.random.default_rng(7)
     for j in rng.integers(0, p.table_bits(), 600):
         j = int(j)
         assert ((int(g[j >> 3]) >> (j & 7)) & 1) == (0 if miller_rabin(p.u + 2 * j) else 1)
+
+
+def test_random_large_geometries_invariants_and_mr(gpu_ctx):
+    """Seeded random (l, f, n) over the whole range up to v < 2^64 (tile
+    sizes, wave counts, ML/far splits and bucket rings all vary): the
+    large-prime invariants hold and Miller-Rabin samples of every table agree."""
+    import paper_1111_3297_b200 as E
+    rng = random.Random(20261020)
+    gpu_ctx.set_max_base_pairs(1 << 28)
+    ran = 0
+    try:
+        for _ in range(12):
+            l = rng.randint(12, 30)
+            nmax = max(1, min(1 << 12, (1 << 31) >> l))  # tables of at most 2^31 bits
+            n = rng.randint(1, nmax)
+            fmax = (((1 << 64) - 1) >> (l + 1)) - n
+            f = rng.randint(max(1, fmax >> rng.randint(0, 40)), fmax)
+            try:
+                p = E.validate_params(l, f, n)
+            except E.Error:
+                continue
+            st = gpu_ctx.count(p, check_invariants=True)
+            g, st2 = gpu_ctx.table(p)
+            assert st.prime_count == st2.prime_count
+            ran += 1
+            for j in np.random.default_rng(l * 1000 + n).integers(0, p.table_bits(), 100):
+                j = int(j)
+                assert ((int(g[j >> 3]) >> (j & 7)) & 1) == (0 if miller_rabin(p.u + 2 * j) else 1), (l, f, n, j)
+    finally:
+        gpu_ctx.set_max_base_pairs(1 << 27)
+    assert ran >= 10
