@@ -44,7 +44,15 @@
   } while (0)
 #endif
 
+#ifndef EG_PLACE_UNROLL
+#define EG_PLACE_UNROLL 2
+#endif
+#ifndef EG_WRITE_UNROLL
+#define EG_WRITE_UNROLL 2
+#endif
+
 namespace eg {
+constexpr int kPlaceUnroll = EG_PLACE_UNROLL, kWriteUnroll = EG_WRITE_UNROLL;
 
 constexpr uint32_t kFull = 0xffffffffu;
 
@@ -1153,7 +1161,7 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
   {
     // placement in tile order (sentinels of idle lanes are skipped)
     const uint32_t rg_a = smem_addr(sm.reg + warp * Sm::R), rk_a = smem_addr(sm.rank + warp * Sm::R);
-#pragma unroll 2
+#pragma unroll kPlaceUnroll
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = lds_u32(rg_a + 4 * i);
       const uint32_t o = lds_u32(off_a + 4 * min(key >> shift, (uint32_t)kScBins - 1));  // sentinels: any bin
@@ -1175,7 +1183,7 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
   }  // (the sinks are never read: their counts may wrap)
   __syncthreads();
   const uint32_t total = sm.total;
-#pragma unroll 2
+#pragma unroll kWriteUnroll
   for (uint32_t i = tid; i < total; i += NT) {
     const uint32_t key = lds_u32(srt_a + 4 * i);
     a.hits[lds_u32(gofs_a + 4 * (key >> shift)) + i] = key & smask;
