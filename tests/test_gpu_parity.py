@@ -389,7 +389,6 @@ def test_near_2p64_far_path_exact(gpu_ctx):
         g, st2 = gpu_ctx.table(p)
     finally:
         gpu_ctx.set_max_base_pairs(1 << 27)
-    assert ran >= 10
     assert st.prime_count == st2.prime_count and st.large_records > 0
     rng = np.random.default_rng(7)
     for j in rng.integers(0, p.table_bits(), 600):
