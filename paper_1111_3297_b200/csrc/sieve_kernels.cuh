@@ -471,10 +471,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         uint32_t p, s;
         uint32_t q = med_first<P2>(cur, t, tf, x_t, combo_a, p, s);
         if ((p << 3) > S) {
+          uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
           while (q < S) {
             mark(tile, q);
-            q += wheel_D(s) * p;
-            s = (s + 1) & 7;
+            q += (dd & 15u) * p;
+            dd = __funnelshift_r(dd, dd, 4);
           }
         } else {
           const uint32_t cp = s_cum[s];
@@ -492,10 +493,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
             mark(tile, q + o7);
           }
           // last partial period: a short wheel walk from class s
+          uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
           while (q < S) {
             mark(tile, q);
-            q += wheel_D(s) * p;
-            s = (s + 1) & 7;
+            q += (dd & 15u) * p;
+            dd = __funnelshift_r(dd, dd, 4);
           }
         }
       }
