@@ -142,3 +142,21 @@ def test_errc_names_match_reference_order(lib):
     for i, name in enumerate(ref_order):  # params.cpp:7-21
         assert lib.erato_gpu_errc_name(i + 1).decode() == name
         assert E.errc_name(E.errc(i)) == name
+
+
+def test_header_flags_and_gpu_errc_match_python_mirror(lib):
+    """The run flags and the GPU-only error codes of include/erato_gpu.h are
+    the ones the Python mirror uses (ordinal + 1 on the ABI)."""
+    import paper_1111_3297_b200 as E
+    from paper_1111_3297_b200 import erato
+    src = open(os.path.join(ROOT, "include", "erato_gpu.h")).read()
+    flags = {m[0]: int(m[1], 16) for m in re.findall(r"#define (ERATO_GPU_\w+) (0x[0-9a-f]+)u", src)}
+    assert flags["ERATO_GPU_TEST_MODE"] == erato.TEST_MODE
+    assert flags["ERATO_GPU_ALLOW_OVERLAP"] == erato.ALLOW_OVERLAP
+    assert flags["ERATO_GPU_CHECK_INVARIANTS"] == erato.CHECK_INVARIANTS
+    codes = {m[0]: int(m[1]) for m in re.findall(r"(ERATO_GPU_E_\w+) = (\d+)", src)}
+    for cname, py in [("ERATO_GPU_E_CUDA", E.errc.cuda_error), ("ERATO_GPU_E_NO_DEVICE", E.errc.no_device),
+                      ("ERATO_GPU_E_INVALID_ARG", E.errc.invalid_argument),
+                      ("ERATO_GPU_E_INVARIANT", E.errc.invariant)]:
+        assert codes[cname] == int(py) + 1
+        assert lib.erato_gpu_errc_name(codes[cname]).decode() == E.errc_name(py)
