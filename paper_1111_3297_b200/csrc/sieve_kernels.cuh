@@ -132,6 +132,17 @@ constexpr uint32_t kPatWords = 11008;  // sum of (M + 96), rounded to a multiple
 __constant__ uint32_t c_gmod[kNumGroups] = {105, 143, 323, 667, 1147, 1763, 2491, 3599};
 __constant__ uint32_t c_goff[kNumGroups] = {0, 201, 440, 859, 1622, 2865, 4724, 7311};  // M + 96 each
 __constant__ uint32_t c_ginv32[kNumGroups] = {23, 76, 212, 271, 466, 1157, 1012, 1912};
+// the same as compile-time constants for unrolled loops (modulo by a
+// constant: multiply-high sequences instead of a division subroutine)
+__host__ __device__ constexpr uint32_t gmod(int k) {
+  return k == 0 ? 105 : k == 1 ? 143 : k == 2 ? 323 : k == 3 ? 667 : k == 4 ? 1147 : k == 5 ? 1763 : k == 6 ? 2491 : 3599;
+}
+__host__ __device__ constexpr uint32_t goff(int k) {
+  return k == 0 ? 0 : k == 1 ? 201 : k == 2 ? 440 : k == 3 ? 859 : k == 4 ? 1622 : k == 5 ? 2865 : k == 6 ? 4724 : 7311;
+}
+__host__ __device__ constexpr uint32_t ginv32(int k) {
+  return k == 0 ? 23 : k == 1 ? 76 : k == 2 ? 212 : k == 3 ? 271 : k == 4 ? 466 : k == 5 ? 1157 : k == 6 ? 1012 : 1912;
+}
 __constant__ uint8_t c_gprimes[kNumGroups][3] = {{3, 5, 7},   {11, 13, 0}, {17, 19, 0}, {23, 29, 0},
                                                  {31, 37, 0}, {41, 43, 0}, {47, 53, 0}, {59, 61, 0}};
 __constant__ uint8_t c_small17[17] = {3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61};
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   __shared__ uint8_t s_combo[64];  // [c'] = adv | cls << 3 (c' = 0..30); [32 + r] = cls of r
   __shared__ uint32_t s_cum[8];
 
-  const uint32_t tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tid = threadIdx.x, bd = kTileThreads, lane = tid & 31, warp = tid >> 5;  // (always launched with kTileThreads)
   const uint32_t log_s = a.log_s;
   const uint32_t S = 1u << log_s, nw = S >> 5;
   const uint64_t t64 = a.tile0 + blockIdx.x;
@@ -326,8 +337,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     uint32_t cur[kNumGroups], stp[kNumGroups];
 #pragma unroll
     for (int k = 0; k < kNumGroups; ++k) {
-      const uint32_t M = c_gmod[k];
-      const uint32_t cg = (uint32_t)((g % M) * c_ginv32[k] % M);
+      const uint32_t M = gmod(k);
+      const uint32_t cg = (uint32_t)((g % M) * ginv32(k) % M);
       cur[k] = (cg + warp * kBlock + lane) % M;
       stp[k] = kStride % M;
     }
@@ -335,13 +346,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
 #pragma unroll
       for (int k = 0; k < kNumGroups; ++k) {
-        const uint32_t* src = pat + c_goff[k] + cur[k];
+        const uint32_t* src = pat + goff(k) + cur[k];
         v0 |= src[0];
         v1 |= src[32];
         v2 |= src[64];
         v3 |= src[96];
         cur[k] += stp[k];
-        if (cur[k] >= c_gmod[k]) cur[k] -= c_gmod[k];
+        if (cur[k] >= gmod(k)) cur[k] -= gmod(k);
       }
       tile[w] = v0;
       tile[w + 32] = v1;
