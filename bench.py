@@ -65,7 +65,7 @@ FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_789_110_090}
 MEDIUM_MARKS = {1: 2_704_493, 2: 2_151_023_657, 3: 673_995_484, 4: 5_391_802_774, 5: 21_567_210_790}
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from `ncu --set full`
 # (profiles/r01_ncu_summary.txt, cfg5 wave 100)
-NCU_TRAFFIC = {5: {"k_tile": 135.7e6 + 3.7e6, "k_scatter_ml": 135.7e6 + 3.7e6, "k_scatter_far": 135.7e6 + 3.7e6}}
+NCU_TRAFFIC = {5: {"k_tile": 135.7e6 + 3.7e6, "k_scatter_ml": 69.5e6 + 113.5e6, "k_scatter_far": 65.1e6 + 42.7e6}}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 R_ATOM_MEASURED = 3.47e12  # smem atomicOr/s per B200, microbench/mb_atomics.cu (profiles/r01_microbench_atomics.log)
 
