@@ -1317,7 +1317,7 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
   const uint32_t nfar = min(*a.far_in_count, a.bcap);
   const uint32_t nw = nblk * kFarWarps;
   const uint32_t nu = (nfar + 31) / 32;
-  const uint64_t left = a.nwaves - a.wave;  // waves from this one to the end
+  const uint32_t left = (uint32_t)min(a.nwaves - a.wave, (uint64_t)0xffffffffu);  // waves from this one to the end
   const uint32_t wofs = warp * FarSmem::R + lane;
   const uint32_t reg_a = smem_addr(sm.reg + warp * FarSmem::R + lane), rank_a = smem_addr(sm.rank + warp * FarSmem::R + lane);
   const uint32_t ent_a = smem_addr(sm.freg + wofs), slot_a = smem_addr(sm.fslot + wofs),
