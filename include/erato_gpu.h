@@ -83,7 +83,17 @@ typedef struct {
   double gen_s;     /* with ERATO_GPU_PHASE_TIMING: ML scatter (k_scatter_ml; k_gen on the fallback) */
   double bin_s;     /* with ERATO_GPU_PHASE_TIMING: far scatter (k_scatter_far; k_bin on the fallback) */
   uint64_t large_records; /* with ERATO_GPU_CHECK_INVARIANTS: hit records consumed by the tiles */
+  double masks_s; /* with ERATO_GPU_PHASE_TIMING: the small-prime pattern phase of the tile kernel
+                     (apply_small_masks, driver.cpp:97-99), %globaltimer in CTA 0 of each launch */
+  uint64_t medium_primes; /* base primes sieved inside the tiles (61 < p <= tile) */
+  uint64_t ml_primes;     /* large primes walked every wave (tile < p <= wave span) */
+  uint64_t far_primes;    /* large primes kept in the per-wave bucket ring (p > wave span) */
 } erato_gpu_stats;
+
+/* Count written to a caller's dev_count when a bucket / hit-list capacity
+ * overflowed (only possible with sync = 0; sync = 1 re-runs with doubled
+ * capacities until the run is exact). */
+#define ERATO_GPU_COUNT_OVERFLOW UINT64_MAX
 
 /* ---- host-side parameter logic (no device needed) ---------------------- */
 
@@ -131,15 +141,35 @@ int erato_gpu_device_count(void);
  *   dev_count  optional device pointer (uint64) receiving the zero-bit count
  *              (lets a caller all-reduce it without a host round trip);
  *   stream     cudaStream_t as void* (NULL = the context's stream);
- *   sync       0: enqueue only, results valid after the stream drains
- *              (stats->prime_count is then NOT filled); 1: wait and fill.
+ *   sync       1: wait, check the capacities (re-running with doubled ones
+ *              after an overflow) and fill stats.
+ *              0: return once every wave is enqueued (one host sync happens
+ *              during init, for the prime-class boundaries); results are
+ *              valid after the stream drains, stats->prime_count is NOT
+ *              filled, and a capacity overflow — which would drop marks —
+ *              is reported on the device: *dev_count = ERATO_GPU_COUNT_OVERFLOW
+ *              (re-run with sync = 1).  ERATO_GPU_CHECK_INVARIANTS needs sync = 1.
  * The interval may be a shard of a larger run; see erato_gpu_shard. */
 int erato_gpu_run(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n, unsigned flags,
                   void* dev_table, uint64_t* dev_count, void* stream, int sync,
                   erato_gpu_stats* stats);
 
+/* SegmentSink equivalent (driver.hpp:34-39): the table is streamed to fn in
+ * order, as contiguous byte slices covering [0, n*2^(l-3)) exactly once
+ * (one slice per wave of tiles, <= ~20 MB), from a library thread while the
+ * next waves sieve.  `bytes` is valid only during the call (it is a pinned
+ * staging slot); a nonzero return aborts the run with ERATO_GPU_IO_ERROR.
+ * Only kOutSlots wave slices are in flight, so neither HBM nor host memory
+ * holds the whole table (the reference's one-segment-at-a-time FileSink,
+ * driver.cpp:29-51). */
+typedef int (*erato_gpu_sink_fn)(void* user, const uint8_t* bytes, uint64_t offset, uint64_t nbytes);
+int erato_gpu_run_to_sink(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                          erato_gpu_sink_fn fn, void* user, erato_gpu_stats* stats);
+
 /* TableSink equivalent (driver.hpp:72-80): the whole table into host memory
- * dst (dst_cap >= n*2^(l-3) bytes). */
+ * dst (dst_cap >= n*2^(l-3) bytes).  Pinned dst: each wave's slice is copied
+ * straight into it while the next waves sieve; pageable dst: through the
+ * pinned staging slots of erato_gpu_run_to_sink. */
 int erato_gpu_sieve_to_host(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n,
                             unsigned flags, uint8_t* dst, size_t dst_cap, erato_gpu_stats* stats);
 
@@ -149,9 +179,13 @@ int erato_gpu_count(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n, unsi
 
 /* FileSink / write_table (driver.hpp:45-58, :98-99): writes
  * out_dir/erato_l{l}_f{f}_n{n}.bits (exactly n*2^(l-3) bytes) and returns
- * the path.  When (part_f, part_n) is a sub-range of (l, f, n) — one shard of
- * a multi-GPU run — only that shard's bytes are pwrite()n at their offset
- * into the shared file; pass part_n = 0 for the whole range. */
+ * the path.  The table is streamed (erato_gpu_run_to_sink + pwrite).
+ *  - (part_f, part_n) == (f, n): the whole table, written to a temporary file
+ *    that is renamed to the reference name only on success.
+ *  - otherwise (part_f, part_n) is one shard of (f, n) (erato_gpu_shard): only
+ *    its bytes are pwrite()n at their offset into the shared file, which is
+ *    created / sized to the full length if needed; part_n = 0 is an empty
+ *    shard (nothing is sieved). */
 int erato_gpu_write_table(erato_gpu_ctx* ctx, const char* out_dir, unsigned l, uint64_t f,
                           uint64_t n, uint64_t part_f, uint64_t part_n, unsigned flags,
                           char* path_out, size_t path_cap, erato_gpu_stats* stats);
@@ -166,6 +200,30 @@ void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_ou
  * Writes up to cap primes to host dst; returns the count in *count. */
 int erato_gpu_extract_primes(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n,
                              unsigned flags, uint64_t* dst, uint64_t cap, uint64_t* count);
+
+/* ---- multi-GPU run_sieve -------------------------------- */
+/* num_gpus contiguous range shards (erato_gpu_shard), one host thread and one
+ * context per shard.  Each shard recomputes its own base primes and offsets
+ * (no data-path collective); the only collective is one
+ * ncclAllReduce(uint64, sum) of the shards' device count words over NVLink /
+ * NVSwitch.  devices: num_gpus CUDA ordinals (NULL = 0..num_gpus-1).  NCCL
+ * (libnccl.so.2, loaded at run time) needs distinct devices; a list that
+ * repeats a device (a test topology on a 1-GPU box) sums the counts on the
+ * host instead — see erato_gpu_multi_uses_nccl. */
+typedef struct erato_gpu_multi erato_gpu_multi;
+int erato_gpu_multi_create(int num_gpus, const int* devices, erato_gpu_multi** out);
+void erato_gpu_multi_destroy(erato_gpu_multi* m);
+int erato_gpu_multi_uses_nccl(const erato_gpu_multi* m);
+/* NullSink run over all shards; *count = the all-reduced count.  stats: device
+ * times are the max over shards, tiles / launches the sum. */
+int erato_gpu_multi_count(erato_gpu_multi* m, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                          uint64_t* count, erato_gpu_stats* stats);
+/* write_table over all shards: each shard streams its bytes into the one
+ * out_dir/erato_l{l}_f{f}_n{n}.bits at its offset (temporary file, renamed
+ * on success). */
+int erato_gpu_multi_write_table(erato_gpu_multi* m, const char* out_dir, unsigned l, uint64_t f,
+                                uint64_t n, unsigned flags, char* path_out, size_t path_cap,
+                                uint64_t* count, erato_gpu_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -74,6 +74,32 @@ __global__ void k_smem_rmw_stride(int iters, uint32_t* out) {
   if (threadIdx.x == 0) out[blockIdx.x] = s[q >> 5 & (WORDS-1)];
 }
 
+// Pure ATOMS issue rate: 16 addresses per thread precomputed in registers,
+// the timed loop is 16 unrolled atomicOr per iteration plus one loop counter
+// (no address arithmetic).  CONFLICT_FREE: lane j always hits bank j (the
+// shared pipe's ceiling); else random words (the sieve's ~3.1-way conflicts).
+template <int WORDS, bool CONFLICT_FREE>
+__global__ void k_smem_atom_pure(int iters, uint32_t* out) {
+  extern __shared__ uint32_t s[];
+  for (int i = threadIdx.x; i < WORDS; i += blockDim.x) s[i] = 0;
+  __syncthreads();
+  uint32_t st = blockIdx.x * 7919u + threadIdx.x * 104729u + 1;
+  uint32_t a[16], m[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t r = lcg(st);
+    const uint32_t w = CONFLICT_FREE ? (((r >> 8) & (WORDS - 1)) & ~31u) | (threadIdx.x & 31) : (r >> 8) & (WORDS - 1);
+    a[k] = (uint32_t)__cvta_generic_to_shared(s + w);
+    m[k] = 1u << (r & 31);
+  }
+  for (int i = 0; i < iters; i += 16) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a[k]), "r"(m[k]) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = s[st & (WORDS - 1)];
+}
+
 // global RED.OR random over a region of `words` words
 __global__ void k_gred(uint32_t* tab, uint64_t words_mask, int iters) {
   uint32_t st = blockIdx.x * 7919u + threadIdx.x * 104729u + 1;
@@ -127,6 +153,12 @@ int main() {
         float t4 = timeit([&] { k_smem_u8_stride<W*4><<<grid, c.threads, sm>>>(iters, out); });
         printf("tile128K thr%d: atom_rand %.3g/s  atom_stride %.3g/s  rmw_stride %.3g/s  u8_stride %.3g/s\n",
                c.threads, ops / t1 * 1e3, ops / t2 * 1e3, ops / t3 * 1e3, ops / t4 * 1e3);
+        CK(cudaFuncSetAttribute(k_smem_atom_pure<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CK(cudaFuncSetAttribute(k_smem_atom_pure<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        float t5 = timeit([&] { k_smem_atom_pure<W, false><<<grid, c.threads, sm>>>(iters, out); });
+        float t6 = timeit([&] { k_smem_atom_pure<W, true><<<grid, c.threads, sm>>>(iters, out); });
+        printf("tile128K thr%d: pure unrolled ATOMS random words %.3g/s  conflict-free %.3g/s\n", c.threads,
+               ops / t5 * 1e3, ops / t6 * 1e3);
       }
     }
     {  // 32 KiB tile (8192 words) — many CTAs/SM

@@ -139,6 +139,10 @@ class Reference:
         L.ref_oracle_bit_table.argtypes = [C.c_uint, C.c_uint64, C.c_uint64, C.c_int, u8p]
         L.ref_f0_table.restype = C.c_int
         L.ref_f0_table.argtypes = [C.c_uint, C.c_uint64, C.c_int, u8p, u64p]
+        L.ref_extract_primes.restype = C.c_int
+        L.ref_extract_primes.argtypes = [C.c_uint, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(u64p), u64p]
+        L.ref_free_u64.restype = None
+        L.ref_free_u64.argtypes = [u64p]
         L.ref_last_error.restype = C.c_char_p
         self.L = L
 
@@ -187,6 +191,16 @@ class Reference:
         cnt = C.c_uint64()
         self._chk(self.L.ref_write_table(out_dir.encode(), l, f, n, int(test_mode), buf, 4096, C.byref(cnt)))
         return buf.value.decode(), cnt.value
+
+    def extract_primes(self, l, f, n, test_mode=False) -> np.ndarray:
+        """run_sieve with the reference PrimeCollectSink (driver.cpp:53-57, :65-81)."""
+        cnt = C.c_uint64()
+        buf = u64p()
+        self._chk(self.L.ref_extract_primes(l, f, n, int(test_mode), C.byref(buf), C.byref(cnt)))
+        try:
+            return np.ctypeslib.as_array(buf, shape=(max(cnt.value, 1),))[:cnt.value].copy()
+        finally:
+            self.L.ref_free_u64(buf)
 
     def oracle_bit_table(self, l, f, n, test_mode=False) -> np.ndarray:
         out = np.zeros((n << l) // 8, dtype=np.uint8)

@@ -13,6 +13,7 @@
 //   simple_sieve           src/oracle.cpp:8-23
 //   oracle_bit_table       src/oracle.cpp:25-46
 //   run_sieve + TableSink/NullSink/FileSink   src/driver.cpp:83-120, :29-63
+//   run_sieve + PrimeCollectSink (extract_primes)   src/driver.cpp:53-57, :65-81
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -133,6 +134,27 @@ int ref_write_table(const char* dir, unsigned l, uint64_t f, uint64_t n, int tes
     return code_of(e);
   }
 }
+
+// PrimeCollectSink run (driver.hpp:62-69, driver.cpp:53-57 / :65-81): the
+// ascending primes of the run in a new[] buffer (*out, free with
+// ref_free_u64), *count = their number.
+int ref_extract_primes(unsigned l, uint64_t f, uint64_t n, int test_mode, uint64_t** out, uint64_t* count) {
+  try {
+    const auto params = erato::validate_params(l, f, n, test_mode != 0);
+    erato::PrimeCollectSink sink;
+    erato::run_sieve(params, sink);
+    const auto& v = sink.primes();
+    *out = new uint64_t[v.size() ? v.size() : 1];
+    if (!v.empty()) std::memcpy(*out, v.data(), v.size() * sizeof(uint64_t));
+    *count = v.size();
+    return 0;
+  } catch (const erato::Error& e) {
+    g_last_error = e.what();
+    return code_of(e);
+  }
+}
+
+void ref_free_u64(uint64_t* p) { delete[] p; }
 
 // The reference's brute-force oracle (v <= 2^40).
 int ref_oracle_bit_table(unsigned l, uint64_t f, uint64_t n, int test_mode, uint8_t* out) {

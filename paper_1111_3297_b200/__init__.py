@@ -6,7 +6,7 @@ include/erato_gpu.h); this package is the host-side mirror of the reference
 interface.  See DESIGN.md.
 """
 from .erato import (  # noqa: F401
-    ALLOW_OVERLAP, TEST_MODE, Context, Error, FileSink, NullSink, PrimeCollectSink, RunOptions, RunStats,
+    ALLOW_OVERLAP, TEST_MODE, Context, Error, FileSink, MultiGPU, NullSink, PrimeCollectSink, RunOptions, RunStats,
     SegmentSink, SieveParams, TableSink, context, decompose_index, device_count, errc, errc_name,
     extract_primes, first_offset, index_to_number, isqrt, number_to_index, params_from_midpoint, run_sieve,
     shard, table_filename, validate_params, write_table,

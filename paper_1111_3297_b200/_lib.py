@@ -21,8 +21,15 @@ EXPORTS = (
     "erato_gpu_table_filename", "erato_gpu_errc_name", "erato_gpu_last_error", "erato_gpu_create",
     "erato_gpu_destroy", "erato_gpu_device_count", "erato_gpu_run", "erato_gpu_sieve_to_host",
     "erato_gpu_count", "erato_gpu_write_table", "erato_gpu_shard", "erato_gpu_extract_primes",
-    "erato_gpu_first_hit", "erato_gpu_set_max_base_pairs",
+    "erato_gpu_first_hit", "erato_gpu_set_max_base_pairs", "erato_gpu_run_to_sink",
+    "erato_gpu_multi_create", "erato_gpu_multi_destroy", "erato_gpu_multi_uses_nccl",
+    "erato_gpu_multi_count", "erato_gpu_multi_write_table",
 )
+
+COUNT_OVERFLOW = (1 << 64) - 1  # ERATO_GPU_COUNT_OVERFLOW
+
+# int (*erato_gpu_sink_fn)(void* user, const uint8_t* bytes, uint64_t offset, uint64_t nbytes)
+SINK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint8), C.c_uint64, C.c_uint64)
 
 
 class Stats(C.Structure):
@@ -34,6 +41,8 @@ class Stats(C.Structure):
         ("log_tile", C.c_uint32), ("waves", C.c_uint32),
         ("kernel_launches", C.c_uint32), ("retries", C.c_uint32),
         ("gen_s", C.c_double), ("bin_s", C.c_double), ("large_records", C.c_uint64),
+        ("masks_s", C.c_double), ("medium_primes", C.c_uint64), ("ml_primes", C.c_uint64),
+        ("far_primes", C.c_uint64),
     ]
 
 
@@ -92,5 +101,20 @@ def load(path: str = SO_PATH):
     L.erato_gpu_extract_primes.restype = C.c_int
     L.erato_gpu_extract_primes.argtypes = [C.c_void_p, C.c_uint, C.c_uint64, C.c_uint64, C.c_uint,
                                            u64p, C.c_uint64, u64p]
+    L.erato_gpu_run_to_sink.restype = C.c_int
+    L.erato_gpu_run_to_sink.argtypes = [C.c_void_p, C.c_uint, C.c_uint64, C.c_uint64, C.c_uint, SINK_FN,
+                                        C.c_void_p, C.POINTER(Stats)]
+    L.erato_gpu_multi_create.restype = C.c_int
+    L.erato_gpu_multi_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]
+    L.erato_gpu_multi_destroy.restype = None
+    L.erato_gpu_multi_destroy.argtypes = [C.c_void_p]
+    L.erato_gpu_multi_uses_nccl.restype = C.c_int
+    L.erato_gpu_multi_uses_nccl.argtypes = [C.c_void_p]
+    L.erato_gpu_multi_count.restype = C.c_int
+    L.erato_gpu_multi_count.argtypes = [C.c_void_p, C.c_uint, C.c_uint64, C.c_uint64, C.c_uint, u64p,
+                                        C.POINTER(Stats)]
+    L.erato_gpu_multi_write_table.restype = C.c_int
+    L.erato_gpu_multi_write_table.argtypes = [C.c_void_p, C.c_char_p, C.c_uint, C.c_uint64, C.c_uint64, C.c_uint,
+                                              C.c_char_p, C.c_size_t, u64p, C.POINTER(Stats)]
     _lib = L
     return L

@@ -6,6 +6,10 @@
 //   erato-gpu sieve  --log-seg 10 --first 2048 --segments 4 --out-dir /tmp
 //   erato-gpu verify --log-seg 12 --first 4096 --segments 8
 //   erato-gpu bench  --exps 12,13,14 --csv bench.csv
+//   erato-gpu sieve  --log-seg 22 --first 137438949376 --segments 8192 --gpus 8
+//
+// --gpus N / --devices D0,D1,..: range shards over several GPUs (one host
+// thread each, counts summed with one ncclAllReduce; erato_gpu_multi_*).
 //
 // Exit codes: 0 success, 1 parameter error, 2 runtime error.  Extension:
 // --allow-overlap admits f = 0 / u^2 <= v (SURVEY.md §8c convention).
@@ -39,6 +43,7 @@ struct Flags {
   std::vector<unsigned> exps;
   std::string csv, machine = "unknown";
   unsigned reps = 3;
+  std::vector<int> devices;  // --gpus / --devices (empty: one GPU, device 0)
 };
 
 [[noreturn]] void usage(const char* msg) {
@@ -46,6 +51,7 @@ struct Flags {
                "error: %s\n"
                "usage: erato-gpu sieve|verify --log-seg L (--first F | --midpoint-exp E) --segments N\n"
                "                 [--test-mode] [--allow-overlap] [--out-dir D] [--count-only] [--max-base-pairs P]\n"
+               "                 [--gpus N | --devices D0,D1,..]\n"
                "       erato-gpu bench --exps E1,E2,.. [--log-seg L] [--csv PATH] [--reps R] [--machine M]\n",
                msg);
   std::exit(1);
@@ -116,6 +122,22 @@ Flags parse(int argc, char** argv) {
       fl.reps = (unsigned)std::max<uint64_t>(1, x);
     } else if (a == "--machine") {
       fl.machine = val();
+    } else if (a == "--gpus") {
+      if (!parse_u64(val(), x) || x < 1 || x > 4096) usage("bad --gpus");
+      fl.devices.clear();
+      for (uint64_t g = 0; g < x; ++g) fl.devices.push_back((int)g);
+    } else if (a == "--devices") {
+      std::string s = val();
+      fl.devices.clear();
+      size_t p = 0;
+      while (p <= s.size()) {
+        const size_t q = s.find(',', p);
+        const std::string tok = s.substr(p, q == std::string::npos ? std::string::npos : q - p);
+        if (!parse_u64(tok.c_str(), x) || x > 4096) usage("bad --devices");
+        fl.devices.push_back((int)x);
+        if (q == std::string::npos) break;
+        p = q + 1;
+      }
     } else if (a == "--kernels") {
       val();  // no GPU counterpart (no multi-backend dispatch)
     } else {
@@ -181,8 +203,8 @@ void print_stats(const erato_gpu_stats& st) {  // print_stats, erato.cpp:75-83
   std::printf("primes    %" PRIu64 "\n", st.prime_count);
   std::printf("segments  %" PRIu64 "\n", st.segments);
   std::printf("init      %.3fs\n", st.init_s);
-  std::printf("masks     %.3fs\n", 0.0);
-  std::printf("medium    %.3fs\n", st.small_s);
+  std::printf("masks     %.3fs\n", st.masks_s);
+  std::printf("medium    %.3fs\n", st.small_s > st.masks_s ? st.small_s - st.masks_s : 0.0);
   std::printf("large     %.3fs\n", st.large_s);
   std::printf("output    %.3fs\n", st.output_s);
 }
@@ -244,19 +266,40 @@ int main(int argc, char** argv) {
   }
   uint64_t u = 0, v = 0;
   if (int rc = erato_gpu_validate(fl.l, f, fl.n, flags, &u, &v)) return report(rc);
-  erato_gpu_ctx* ctx = nullptr;
-  if (int rc = erato_gpu_create(0, &ctx)) return report(rc);
-  erato_gpu_set_max_base_pairs(ctx, fl.max_base_pairs);
   erato_gpu_stats st{};
   int rc = 0;
-  if (fl.cmd == "sieve") {
+  // per-phase device times for print_stats (masks / medium / large)
+  const unsigned run_flags = flags | ERATO_GPU_PHASE_TIMING;
+  if (fl.cmd == "sieve" && fl.devices.size() > 1) {  // range shards over several GPUs
+    erato_gpu_multi* m = nullptr;
+    if ((rc = erato_gpu_multi_create((int)fl.devices.size(), fl.devices.data(), &m))) return report(rc);
+    uint64_t cnt = 0;
     if (fl.count_only) {
-      uint64_t cnt = 0;
-      rc = erato_gpu_count(ctx, fl.l, f, fl.n, flags, &cnt, &st);
+      rc = erato_gpu_multi_count(m, fl.l, f, fl.n, run_flags, &cnt, &st);
       if (!rc) print_stats(st);
     } else {
       char path[4096];
-      rc = erato_gpu_write_table(ctx, fl.out_dir.c_str(), fl.l, f, fl.n, 0, 0, flags, path, sizeof(path), &st);
+      rc = erato_gpu_multi_write_table(m, fl.out_dir.c_str(), fl.l, f, fl.n, run_flags, path, sizeof(path), &cnt, &st);
+      if (!rc) {
+        print_stats(st);
+        std::printf("table     %s (%" PRIu64 " bytes)\n", path, (fl.n << fl.l) / 8);
+      }
+    }
+    erato_gpu_multi_destroy(m);
+    if (rc) return report(rc);
+    return 0;
+  }
+  erato_gpu_ctx* ctx = nullptr;
+  if ((rc = erato_gpu_create(fl.devices.empty() ? 0 : fl.devices[0], &ctx))) return report(rc);
+  erato_gpu_set_max_base_pairs(ctx, fl.max_base_pairs);
+  if (fl.cmd == "sieve") {
+    if (fl.count_only) {
+      uint64_t cnt = 0;
+      rc = erato_gpu_count(ctx, fl.l, f, fl.n, run_flags, &cnt, &st);
+      if (!rc) print_stats(st);
+    } else {
+      char path[4096];
+      rc = erato_gpu_write_table(ctx, fl.out_dir.c_str(), fl.l, f, fl.n, f, fl.n, run_flags, path, sizeof(path), &st);
       if (!rc) {
         print_stats(st);
         std::printf("table     %s (%" PRIu64 " bytes)\n", path, (fl.n << fl.l) / 8);

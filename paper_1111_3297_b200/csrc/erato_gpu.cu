@@ -15,16 +15,22 @@
 //     (patterns, medium primes, hits, popcount, 128-bit write-out)
 //   count: device u64 (NullSink: only it leaves the device).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <fcntl.h>
+#include <nccl.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/erato_gpu.h"
@@ -86,6 +92,7 @@ uint64_t pi_upper(uint64_t x) {
 constexpr uint32_t kBaseLogTile = 20;  // tile size for the sieve of [1, sqrt(v)]
 constexpr uint32_t kGenBlocksPerSm = 2;
 constexpr uint64_t kFewLarge = 2048;  // at most this many primes > S are sieved as medium primes
+constexpr int kOutSlots = 4;          // streaming output: wave slices in flight (device and pinned host)
 
 }  // namespace
 
@@ -105,6 +112,17 @@ struct erato_gpu_ctx {
   uint64_t max_base_pairs = uint64_t{1} << 27;  // base.hpp:87
   cudaEvent_t ev[4] = {};
   std::vector<cudaEvent_t> phase_ev;  // pairs, grown on demand
+  // streaming output (run_to_sink, sieve_to_host, write_table): a ring of
+  // kOutSlots wave slices on the device and in pinned host memory, so no
+  // call needs the whole table in HBM or in host memory
+  DevBuf slices;
+  uint8_t* hslots = nullptr;
+  size_t hslots_cap = 0;
+  uint64_t* hflags = nullptr;  // pinned [kOutSlots]: overflow flag as of each slot's wave
+  cudaEvent_t ev_copy[kOutSlots] = {};
+  // extract_primes: the last compaction, reused by a follow-up call with the same key
+  uint64_t xp_key[4] = {~0ull, ~0ull, ~0ull, ~0ull};
+  uint64_t xp_count = 0;
 };
 
 extern "C" {
@@ -230,14 +248,10 @@ int erato_gpu_device_count(void) {
   return n;
 }
 
-int erato_gpu_create(int device, erato_gpu_ctx** out) {
-  if (!out) return fail(ERATO_GPU_E_INVALID_ARG, "out is NULL");
-  *out = nullptr;
-  if (erato_gpu_device_count() == 0) return fail(ERATO_GPU_E_NO_DEVICE, "no CUDA device visible");
-  if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+namespace {
+int create_impl(erato_gpu_ctx* c) {
+  const int device = c->device;
   CUDA_TRY(cudaSetDevice(device));
-  auto* c = new erato_gpu_ctx();
-  c->device = device;
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   c->nsm = prop.multiProcessorCount;
@@ -246,6 +260,12 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   CUDA_TRY(cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&c->xjoin, cudaEventDisableTiming));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  for (auto& e : c->ev_copy) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_TRY(cudaMallocHost(&c->hflags, kOutSlots * sizeof(uint64_t)));
+  if (const char* e = std::getenv("ERATO_GPU_TEST_CAP_SCALE")) {  // tests only: force capacity overflows
+    const double v = std::atof(e);
+    if (v > 0) c->hcap_scale = c->bcap_scale = v;
+  }
   for (auto kt : {eg::k_tile<false, false>, eg::k_tile<true, false>, eg::k_tile<false, true>, eg::k_tile<true, true>})
     CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(eg::kPatWords * 4 + (1u << kBaseLogTile) / 8 + eg::kMaxWarpPrimes * 8 +
@@ -273,6 +293,24 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
   CUDA_TRY(cudaMemcpyAsync(c->h_sp.data(), c->sp.p, nsp * 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
+int erato_gpu_create(int device, erato_gpu_ctx** out) {
+  if (!out) return fail(ERATO_GPU_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (erato_gpu_device_count() == 0) return fail(ERATO_GPU_E_NO_DEVICE, "no CUDA device visible");
+  if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+  auto* c = new erato_gpu_ctx();
+  c->device = device;
+  const int rc = create_impl(c);
+  if (rc) {  // release whatever was created before the failure
+    const std::string msg = g_err;
+    erato_gpu_destroy(c);
+    g_err = msg;
+    return rc;
+  }
   *out = c;
   return 0;
 }
@@ -280,17 +318,24 @@ int erato_gpu_create(int device, erato_gpu_ctx** out) {
 void erato_gpu_destroy(erato_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->xstream) cudaStreamSynchronize(c->xstream);
   for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
-                    &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount})
+                    &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount, &c->slices})
     b->release();
+  if (c->hslots) cudaFreeHost(c->hslots);
+  if (c->hflags) cudaFreeHost(c->hflags);
   for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_copy)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->phase_ev) cudaEventDestroy(e);
   if (c->xev) cudaEventDestroy(c->xev);
   if (c->xjoin) cudaEventDestroy(c->xjoin);
   if (c->xstream) cudaStreamDestroy(c->xstream);
   if (c->stream) cudaStreamDestroy(c->stream);
+  cudaGetLastError();
   delete c;
 }
 
@@ -353,11 +398,120 @@ struct Plan {
 }  // namespace
 
 namespace {
-// host_dst (pinned, optional): each wave's finished slice of dev_table is
-// copied to host_dst on a side stream while the next waves run.
+
+__global__ void k_finish(const unsigned long long* __restrict__ count, const uint64_t* __restrict__ overflow,
+                         uint64_t* __restrict__ out) {
+  *out = *overflow ? ERATO_GPU_COUNT_OVERFLOW : (uint64_t)*count;
+}
+
+// Streaming output of finished waves (the FileSink / TableSink analog that
+// never holds the whole table): wave w's tiles write device slice w % K; the
+// slice goes D2H on the copy stream while the next waves sieve, either
+// straight into a pinned whole-table destination (host_dst) or into pinned
+// slot w % K, which a writer thread hands to fn in order.  A wave is handed
+// over only if the overflow flag, copied with it, is clear; after a
+// capacity retry the waves already delivered (delivered bytes) are skipped,
+// so fn sees every byte exactly once, in order.
+struct OutSpec {
+  uint8_t* host_dst = nullptr;
+  erato_gpu_sink_fn fn = nullptr;
+  void* user = nullptr;
+  uint64_t delivered = 0;  // bytes handed to fn so far (survives retries)
+};
+
+struct WaveJob {
+  uint32_t slot;
+  uint64_t b0, nbytes;
+};
+
+struct Writer {
+  erato_gpu_ctx* c = nullptr;
+  OutSpec* out = nullptr;
+  size_t slice_bytes = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  std::deque<WaveJob> q;
+  bool closing = false;
+  uint64_t consumed = 0;  // waves taken off the queue and finished with
+  int err = 0;            // first failure (ERATO_GPU_IO_ERROR / E_CUDA)
+  bool overflow = false;  // a wave arrived with the overflow flag set
+  std::string msg;
+  std::thread th;
+
+  ~Writer() { finish(); }  // early error returns of run_impl still join the thread
+  void start() {
+    th = std::thread([this] { loop(); });
+  }
+  void push(const WaveJob& j) {
+    std::lock_guard<std::mutex> g(m);
+    q.push_back(j);
+    cv.notify_all();
+  }
+  // block until at least `waves` waves are consumed; false if the run must stop
+  bool wait_consumed(uint64_t waves) {
+    std::unique_lock<std::mutex> g(m);
+    cv.wait(g, [&] { return consumed >= waves || err || overflow; });
+    return !(err || overflow);
+  }
+  void finish() {
+    {
+      std::lock_guard<std::mutex> g(m);
+      closing = true;
+      cv.notify_all();
+    }
+    if (th.joinable()) th.join();
+  }
+  void loop() {
+    cudaSetDevice(c->device);
+    for (;;) {
+      WaveJob j;
+      {
+        std::unique_lock<std::mutex> g(m);
+        cv.wait(g, [&] { return !q.empty() || closing; });
+        if (q.empty()) return;
+        j = q.front();
+        q.pop_front();
+      }
+      int e = 0;
+      bool ovf = false;
+      std::string why;
+      const bool stop = err || overflow;
+      if (!stop) {
+        const cudaError_t ce = cudaEventSynchronize(c->ev_copy[j.slot]);
+        if (ce != cudaSuccess) {
+          e = ERATO_GPU_E_CUDA;
+          why = std::string("copy of a finished wave: ") + cudaGetErrorString(ce);
+        } else if (c->hflags[j.slot]) {
+          ovf = true;
+        } else if (j.b0 + j.nbytes > out->delivered) {
+          const uint64_t skip = out->delivered > j.b0 ? out->delivered - j.b0 : 0;
+          const uint8_t* src = c->hslots + (size_t)j.slot * slice_bytes + skip;
+          if (out->fn(out->user, src, j.b0 + skip, j.nbytes - skip) != 0) {
+            e = ERATO_GPU_IO_ERROR;
+            why = "sink rejected bytes at offset " + std::to_string(j.b0 + skip);
+          } else {
+            out->delivered = j.b0 + j.nbytes;
+          }
+        }
+      }
+      std::lock_guard<std::mutex> g(m);
+      if (e && !err) {
+        err = e;
+        msg = why;
+      }
+      if (ovf) overflow = true;
+      ++consumed;
+      cv.notify_all();
+    }
+  }
+};
+
 int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags, void* dev_table,
-             uint64_t* dev_count, void* stream_v, int sync, erato_gpu_stats* stats, uint8_t* host_dst) {
+             uint64_t* dev_count, void* stream_v, int sync, erato_gpu_stats* stats, OutSpec* out) {
   if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
+  if (!sync && (flags & ERATO_GPU_CHECK_INVARIANTS))
+    return fail(ERATO_GPU_E_INVALID_ARG, "ERATO_GPU_CHECK_INVARIANTS needs sync = 1 (the checks are read on the host)");
+  if (out && (dev_table || !sync)) return fail(ERATO_GPU_E_INVALID_ARG, "streaming output is synchronous and owns the table");
   Plan P{};
   int rc = erato_gpu_validate(l, f, n, flags, &P.u, &P.v);
   if (rc) return rc;
@@ -408,7 +562,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     const uint64_t prime_cap = pi_upper(vroot) + 64;
     CUDA_TRY(c->primes.ensure(prime_cap * 4));
     // [0] total primes, [8..15] bounds + largest prime, [16] count, [17] overflow,
-    // [18] hit records consumed, [19] expected records, [20] base-sieve count, [21] bad far entry
+    // [18] hit records consumed, [19] expected records, [20] base-sieve count, [21] bad far entry,
+    // [22] pattern-phase ns (PHASE_TIMING), [24..30] class thresholds, [40] compaction total
     uint64_t* d_scal = c->scal.as<uint64_t>();
     CUDA_TRY(cudaMemsetAsync(d_scal + 18, 0, 16, st));
     CUDA_TRY(cudaMemsetAsync(d_scal + 21, 0, 8, st));
@@ -563,8 +718,35 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     ta.hitcnt = c->hitcnt.as<uint32_t>();
     ta.hcap = hcap;
     ta.table = static_cast<uint32_t*>(dev_table);
+    // streaming output: K wave slices on the device (+ pinned slots for a sink)
+    const uint64_t slice_bytes = std::min<uint64_t>((uint64_t)P.W << P.log_s, P.T) / 8;
+    Writer wr;
+    if (out) {
+      CUDA_TRY(c->slices.ensure(((slice_bytes + 15) & ~15ull) * kOutSlots));
+      if (out->fn && c->hslots_cap < slice_bytes * kOutSlots) {
+        if (c->hslots) cudaFreeHost(c->hslots);
+        c->hslots = nullptr;
+        c->hslots_cap = 0;
+        CUDA_TRY(cudaMallocHost(&c->hslots, slice_bytes * kOutSlots));
+        c->hslots_cap = slice_bytes * kOutSlots;
+      }
+      if (out->fn) {
+        wr.c = c;
+        wr.out = out;
+        wr.slice_bytes = slice_bytes;
+        wr.start();
+      }
+    }
+    auto stop_writer = [&]() {
+      if (out && out->fn) wr.finish();
+    };
     ta.count = d_count;
     ta.tbase = 0;
+    const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
+    if (timing) {
+      CUDA_TRY(cudaMemsetAsync(d_scal + 22, 0, 8, st));
+      ta.phase_ns = reinterpret_cast<unsigned long long*>(d_scal + 22);
+    }
     const uint32_t gen_blocks = (uint32_t)c->nsm * kGenBlocksPerSm;
     const uint32_t gen_warps = gen_blocks * (eg::kGenThreads / 32);
     const uint32_t bin_blocks = std::max<uint32_t>((uint32_t)c->nsm * 2, (gen_warps + eg::kMaxRegionsPerCta - 1) / eg::kMaxRegionsPerCta);
@@ -645,7 +827,6 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       sca.hcap = hcap;
       sca.overflow = ga.overflow;
     }
-    const bool timing = (flags & ERATO_GPU_PHASE_TIMING) != 0;
     const size_t nev = timing ? (size_t)P.nwaves * 5 + 8 : 0;
     while (c->phase_ev.size() < nev) {
       cudaEvent_t e;
@@ -716,6 +897,13 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         }
       }
       ta.tile0 = tile0;
+      const uint32_t oslot = (uint32_t)(w % kOutSlots);
+      if (out) {  // this wave's tiles go to slice oslot once its previous wave has left it
+        if (out->fn && w >= kOutSlots && !wr.wait_consumed(w - kOutSlots + 1)) break;
+        if (w >= kOutSlots) CUDA_TRY(cudaStreamWaitEvent(st, c->ev_copy[oslot], 0));
+        ta.table = reinterpret_cast<uint32_t*>(c->slices.as<uint8_t>() + (size_t)oslot * ((slice_bytes + 15) & ~15ull));
+        ta.out_tile0 = tile0;
+      }
       if (tile0 + ntw - ta.tbase > eg::kMaxChunkTiles && nmed) {
         // new chunk: medium records for tile indices relative to tile0 (< 2^22)
         ta.tbase = tile0;
@@ -726,12 +914,16 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       }
       if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
       launch_tiles(st, ta, ntw, P.overlap);
-      if (host_dst && dev_table) {  // output pipeline: this wave's bytes go to the host now
+      if (out) {  // output pipeline: this wave's bytes go to the host now
         const uint64_t b0 = (tile0 << P.log_s) / 8, b1 = std::min<uint64_t>((tile0 + ntw) << P.log_s, P.T) / 8;
         CUDA_TRY(cudaEventRecord(c->xev, st));
         CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->xev, 0));
-        CUDA_TRY(cudaMemcpyAsync(host_dst + b0, static_cast<uint8_t*>(dev_table) + b0, b1 - b0,
-                                 cudaMemcpyDeviceToHost, c->xstream));
+        uint8_t* dst = out->fn ? c->hslots + (size_t)oslot * slice_bytes : out->host_dst + b0;
+        CUDA_TRY(cudaMemcpyAsync(dst, ta.table, b1 - b0, cudaMemcpyDeviceToHost, c->xstream));
+        if (out->fn)
+          CUDA_TRY(cudaMemcpyAsync(c->hflags + oslot, d_scal + 17, 8, cudaMemcpyDeviceToHost, c->xstream));
+        CUDA_TRY(cudaEventRecord(c->ev_copy[oslot], c->xstream));
+        if (out->fn) wr.push(WaveJob{oslot, b0, b1 - b0});
       }
       if (timing) {
         CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
@@ -740,12 +932,14 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       }
       ++launches;
     }
-    if (host_dst && dev_table) {  // join the copies
+    if (out) {  // join the copies
       CUDA_TRY(cudaEventRecord(c->xjoin, c->xstream));
       CUDA_TRY(cudaStreamWaitEvent(st, c->xjoin, 0));
     }
     CUDA_TRY(cudaGetLastError());
-    if (dev_count) CUDA_TRY(cudaMemcpyAsync(dev_count, d_count, 8, cudaMemcpyDeviceToDevice, st));
+    // the caller's count, or ERATO_GPU_COUNT_OVERFLOW if a capacity overflowed
+    // (visible on the device without a host sync when sync = 0)
+    if (dev_count) k_finish<<<1, 1, 0, st>>>(d_count, d_scal + 17, dev_count);
     CUDA_TRY(cudaEventRecord(c->ev[2], st));
     if (!sync) {
       if (stats) {
@@ -759,9 +953,14 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       }
       return 0;  // overflow cannot be checked without a sync; capacities are generous
     }
-    uint64_t res[6];  // d_scal[16..21]
+    uint64_t res[7];  // d_scal[16..22]
     CUDA_TRY(cudaMemcpyAsync(res, d_scal + 16, sizeof(res), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    const cudaError_t se = cudaStreamSynchronize(st);
+    stop_writer();
+    if (se != cudaSuccess) return fail(ERATO_GPU_E_CUDA, std::string("run: ") + cudaGetErrorString(se));
+    if (out && out->fn && wr.err) return fail(wr.err, wr.msg);
+    if (out && out->fn && !wr.overflow && out->delivered != P.T / 8 && !res[1])
+      return fail(ERATO_GPU_E_CUDA, "streaming output incomplete");
     if ((int)res[1] != 0) {
       if (attempt >= 4) return fail(ERATO_GPU_ALLOC_LIMIT, "bucket capacity overflow persists");
       c->hcap_scale *= 2.0;
@@ -803,11 +1002,15 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           }
         }
         stats->gen_s = tg * 1e-3;
+        stats->masks_s = (double)res[6] * 1e-9;
         stats->bin_s = tb * 1e-3;
         stats->small_s = ts * 1e-3;
         stats->large_s = tl * 1e-3;
       }
       stats->total_s = t_tot * 1e-3;
+      stats->medium_primes = nmed;
+      stats->ml_primes = nml;
+      stats->far_primes = nfar;
       stats->base_primes = nprimes;
       stats->tiles = P.ntiles;
       stats->log_tile = P.log_s;
@@ -837,6 +1040,28 @@ extern "C" int erato_gpu_count(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_
   return 0;
 }
 
+extern "C" int erato_gpu_run_to_sink(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                                     erato_gpu_sink_fn fn, void* user, erato_gpu_stats* stats) {
+  if (!c || !fn) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
+  erato_gpu_stats local{};
+  erato_gpu_stats* s = stats ? stats : &local;
+  std::memset(s, 0, sizeof(*s));
+  OutSpec o;
+  o.fn = fn;
+  o.user = user;
+  return run_impl(c, l, f, n, flags, nullptr, nullptr, nullptr, 1, s, &o);
+}
+
+namespace {
+struct HostCopy {
+  uint8_t* dst;
+};
+int host_copy_fn(void* user, const uint8_t* bytes, uint64_t offset, uint64_t nbytes) {
+  std::memcpy(static_cast<HostCopy*>(user)->dst + offset, bytes, nbytes);
+  return 0;
+}
+}  // namespace
+
 extern "C" int erato_gpu_sieve_to_host(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flags,
                                        uint8_t* dst, size_t dst_cap, erato_gpu_stats* stats) {
   if (!c || !dst) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
@@ -845,26 +1070,59 @@ extern "C" int erato_gpu_sieve_to_host(erato_gpu_ctx* c, unsigned l, uint64_t f,
   const uint64_t bytes = (n << l) / 8;
   if (dst_cap < bytes) return fail(ERATO_GPU_E_INVALID_ARG, "dst_cap < table bytes");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(c->table.ensure((bytes + 15) & ~15ull));
   erato_gpu_stats local{};
   erato_gpu_stats* s = stats ? stats : &local;
   std::memset(s, 0, sizeof(*s));
-  // pinned destination: copy each wave's slice while the next waves run
+  // pinned destination: each wave's slice is copied straight into it while
+  // the next waves run; pageable: through the pinned slots
   cudaPointerAttributes pa{};
   const bool pinned = cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   cudaGetLastError();
-  rc = run_impl(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, s, pinned ? dst : nullptr);
-  if (rc) return rc;
-  if (pinned) return 0;  // (output_s stays 0: the copies overlapped the sieve)
-  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
-  CUDA_TRY(cudaMemcpyAsync(dst, c->table.p, bytes, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  float ms = 0;
-  cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]);
-  s->output_s = ms * 1e-3;
+  OutSpec o;
+  HostCopy hc{dst};
+  if (pinned) {
+    o.host_dst = dst;
+  } else {
+    o.fn = host_copy_fn;
+    o.user = &hc;
+  }
+  return run_impl(c, l, f, n, flags, nullptr, nullptr, nullptr, 1, s, &o);
+}
+
+namespace {
+struct FileOut {
+  int fd;
+  uint64_t base;  // byte offset of this shard in the file
+};
+int pwrite_fn(void* user, const uint8_t* bytes, uint64_t offset, uint64_t nbytes) {
+  auto* fo = static_cast<FileOut*>(user);
+  uint64_t done = 0;
+  while (done < nbytes) {
+    const ssize_t w = ::pwrite(fo->fd, bytes + done, (size_t)std::min<uint64_t>(nbytes - done, 1ull << 30),
+                               (off_t)(fo->base + offset + done));
+    if (w <= 0) return 1;
+    done += (uint64_t)w;
+  }
   return 0;
 }
+
+// FileSink: create_directories + exact name (driver.cpp:17-36)
+std::string table_path(const char* out_dir, unsigned l, uint64_t f, uint64_t n) {
+  std::string dir(out_dir);
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0777);
+  char name[128];
+  erato_gpu_table_filename(l, f, n, name, sizeof(name));
+  return dir + (dir.empty() || dir.back() == '/' ? "" : "/") + name;
+}
+
+// Stream the shard (part_f, part_n) of (l, f, n) into fd at its byte offset.
+int write_shard(erato_gpu_ctx* c, int fd, unsigned l, uint64_t f, uint64_t part_f, uint64_t part_n,
+                unsigned flags, erato_gpu_stats* stats) {
+  FileOut fo{fd, ((part_f - f) << l) / 8};
+  return erato_gpu_run_to_sink(c, l, part_f, part_n, flags, pwrite_fn, &fo, stats);
+}
+}  // namespace
 
 extern "C" int erato_gpu_write_table(erato_gpu_ctx* c, const char* out_dir, unsigned l, uint64_t f, uint64_t n,
                                      uint64_t part_f, uint64_t part_n, unsigned flags, char* path_out,
@@ -872,55 +1130,38 @@ extern "C" int erato_gpu_write_table(erato_gpu_ctx* c, const char* out_dir, unsi
   if (!c || !out_dir) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
   int rc = erato_gpu_validate(l, f, n, flags, nullptr, nullptr);
   if (rc) return rc;
-  if (part_n == 0) {
-    part_f = f;
-    part_n = n;
-  }
-  if (part_f < f || part_f + part_n > f + n) return fail(ERATO_GPU_E_INVALID_ARG, "part outside (f, n)");
-  // FileSink: create_directories + exact name (driver.cpp:29-36)
-  std::string dir(out_dir);
-  for (size_t i = 1; i <= dir.size(); ++i)
-    if (i == dir.size() || dir[i] == '/') ::mkdir(dir.substr(0, i).c_str(), 0777);
-  char name[128];
-  erato_gpu_table_filename(l, f, n, name, sizeof(name));
-  const std::string path = dir + (dir.empty() || dir.back() == '/' ? "" : "/") + name;
-  const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT, 0644);
-  if (fd < 0) return fail(ERATO_GPU_IO_ERROR, "cannot open " + path);
+  if (part_f < f || part_n > n || part_f - f > n - part_n) return fail(ERATO_GPU_E_INVALID_ARG, "part outside (f, n)");
+  const std::string path = table_path(out_dir, l, f, n);
   const uint64_t total_bytes = (n << l) / 8;
+  if (stats) std::memset(stats, 0, sizeof(*stats));
   if (part_f == f && part_n == n) {
-    if (::ftruncate(fd, (off_t)total_bytes) != 0) {
+    // whole table: stream into a temporary file, rename on success (a failed
+    // run never leaves a table at the reference name)
+    const std::string tmp = path + ".tmp." + std::to_string(::getpid());
+    const int fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) return fail(ERATO_GPU_IO_ERROR, "cannot open " + tmp);
+    rc = write_shard(c, fd, l, f, f, n, flags, stats);
+    if (!rc && ::ftruncate(fd, (off_t)total_bytes) != 0) rc = fail(ERATO_GPU_IO_ERROR, "truncate failed for " + tmp);
+    if (::close(fd) != 0 && !rc) rc = fail(ERATO_GPU_IO_ERROR, "close failed for " + tmp);
+    if (!rc && ::rename(tmp.c_str(), path.c_str()) != 0) rc = fail(ERATO_GPU_IO_ERROR, "rename to " + path + " failed");
+    if (rc) {
+      ::unlink(tmp.c_str());
+      return rc;
+    }
+  } else {
+    // one shard of a multi-GPU run: pwrite at its offset into the shared file
+    // (part_n == 0: an empty shard, nothing to sieve)
+    const int fd = ::open(path.c_str(), O_WRONLY | O_CREAT, 0644);
+    if (fd < 0) return fail(ERATO_GPU_IO_ERROR, "cannot open " + path);
+    if (::ftruncate(fd, (off_t)total_bytes) != 0) {  // idempotent across shards
       ::close(fd);
       return fail(ERATO_GPU_IO_ERROR, "truncate failed for " + path);
     }
+    if (part_n) rc = write_shard(c, fd, l, f, part_f, part_n, flags, stats);
+    if (::close(fd) != 0 && !rc) rc = fail(ERATO_GPU_IO_ERROR, "close failed for " + path);
+    if (rc) return rc;
   }
-  const uint64_t bytes = (part_n << l) / 8;
-  const uint64_t off = ((part_f - f) << l) / 8;
-  std::vector<uint8_t> host;
-  uint8_t* pinned = nullptr;
-  if (cudaMallocHost(&pinned, bytes ? bytes : 1) != cudaSuccess) {
-    cudaGetLastError();
-    pinned = nullptr;
-    host.resize(bytes);
-  }
-  uint8_t* dst = pinned ? pinned : host.data();
-  rc = erato_gpu_sieve_to_host(c, l, part_f, part_n, flags, dst, bytes, stats);
-  if (rc) {
-    if (pinned) cudaFreeHost(pinned);
-    ::close(fd);
-    return rc;
-  }
-  uint64_t done = 0;
-  while (done < bytes) {
-    const ssize_t w = ::pwrite(fd, dst + done, (size_t)std::min<uint64_t>(bytes - done, 1ull << 30), (off_t)(off + done));
-    if (w <= 0) {
-      if (pinned) cudaFreeHost(pinned);
-      ::close(fd);
-      return fail(ERATO_GPU_IO_ERROR, "short write to " + path);
-    }
-    done += (uint64_t)w;
-  }
-  if (pinned) cudaFreeHost(pinned);
-  if (::close(fd) != 0) return fail(ERATO_GPU_IO_ERROR, "close failed for " + path);
+  if (stats) stats->segments = part_n;
   if (path_out && path_cap) std::snprintf(path_out, path_cap, "%s", path.c_str());
   return 0;
 }
@@ -932,22 +1173,278 @@ extern "C" int erato_gpu_extract_primes(erato_gpu_ctx* c, unsigned l, uint64_t f
   int rc = erato_gpu_validate(l, f, n, flags, &u, &v);
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(c->device));
-  const uint64_t T = n << l;
-  CUDA_TRY(c->table.ensure(((T / 8) + 15) & ~15ull));
-  erato_gpu_stats s{};
-  rc = erato_gpu_run(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, &s);
-  if (rc) return rc;
-  // the number 1 (bit 0 of an f = 0 run) is a clear bit but not a prime
-  const uint64_t lo = (u == 1) ? 1 : 0;
-  const uint64_t np = s.prime_count - lo;
-  CUDA_TRY(c->outbuf.ensure(std::max<uint64_t>(np, 1) * 8));
-  uint64_t* d_total = c->scal.as<uint64_t>() + 40;
-  // extract_primes (driver.cpp:65-81): clear bits -> u + 2j
-  rc = compact_zeros<uint64_t>(c, c->stream, c->table.as<uint32_t>(), T, lo, u, c->outbuf.as<uint64_t>(), np, d_total);
-  if (rc) return rc;
+  const uint64_t key[4] = {l, f, n, flags};
+  if (!std::equal(key, key + 4, c->xp_key)) {
+    // sieve + compaction once; a follow-up call with the same (l, f, n, flags)
+    // (e.g. the first to learn the count, the second with a buffer) only copies
+    std::fill(c->xp_key, c->xp_key + 4, ~0ull);
+    const uint64_t T = n << l;
+    CUDA_TRY(c->table.ensure(((T / 8) + 15) & ~15ull));
+    erato_gpu_stats s{};
+    rc = erato_gpu_run(c, l, f, n, flags, c->table.p, nullptr, nullptr, 1, &s);
+    if (rc) return rc;
+    // the number 1 (bit 0 of an f = 0 run) is a clear bit but not a prime
+    const uint64_t lo = (u == 1) ? 1 : 0;
+    const uint64_t np0 = s.prime_count - lo;
+    CUDA_TRY(c->outbuf.ensure(std::max<uint64_t>(np0, 1) * 8));
+    uint64_t* d_total = c->scal.as<uint64_t>() + 40;
+    // extract_primes (driver.cpp:65-81): clear bits -> u + 2j
+    rc = compact_zeros<uint64_t>(c, c->stream, c->table.as<uint32_t>(), T, lo, u, c->outbuf.as<uint64_t>(), np0,
+                                 d_total);
+    if (rc) return rc;
+    uint64_t written = 0;
+    CUDA_TRY(cudaMemcpyAsync(&written, d_total, 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (written != np0)
+      return fail(ERATO_GPU_E_INVARIANT, "compaction wrote " + std::to_string(written) + " primes, count says " +
+                                             std::to_string(np0));
+    c->xp_count = np0;
+    std::copy(key, key + 4, c->xp_key);
+  }
+  const uint64_t np = c->xp_count;
   const uint64_t m = std::min(np, cap);
   if (dst && m) CUDA_TRY(cudaMemcpyAsync(dst, c->outbuf.p, m * 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (count) *count = np;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU run_sieve: contiguous range shards, one host
+// thread per shard driving its device, and one collective — the sum of the
+// per-shard counts, ncclAllReduce(uint64, sum) over NVLink between the
+// devices' count words.  NCCL is loaded at run time (libnccl.so.2): the
+// library has no link-time NCCL dependency, and a process that already
+// loaded torch's NCCL shares it.
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"})
+      if ((h = ::dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) {
+      api.why = std::string("cannot load libnccl.so.2: ") + ::dlerror();
+      return;
+    }
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(::dlsym(h, "ncclCommInitAll"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(::dlsym(h, "ncclCommDestroy"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(::dlsym(h, "ncclAllReduce"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(::dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(::dlsym(h, "ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(::dlsym(h, "ncclGetErrorString"));
+    api.ok = api.CommInitAll && api.CommDestroy && api.AllReduce && api.GroupStart && api.GroupEnd && api.GetErrorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a needed symbol";
+  });
+  return api;
+}
+
+}  // namespace
+
+struct erato_gpu_multi {
+  int num = 0;
+  std::vector<int> devices;
+  std::vector<erato_gpu_ctx*> ctx;
+  std::vector<uint64_t*> dcount;  // one count word per shard, on its device
+  std::vector<ncclComm_t> comms;  // empty: devices repeat (test topology), counts summed on the host
+};
+
+extern "C" void erato_gpu_multi_destroy(erato_gpu_multi* m) {
+  if (!m) return;
+  if (!m->comms.empty() && nccl().ok)
+    for (auto cm : m->comms) nccl().CommDestroy(cm);
+  for (int g = 0; g < (int)m->ctx.size(); ++g) {
+    if (m->dcount[g]) {
+      cudaSetDevice(m->devices[g]);
+      cudaFree(m->dcount[g]);
+    }
+    erato_gpu_destroy(m->ctx[g]);
+  }
+  cudaGetLastError();
+  delete m;
+}
+
+extern "C" int erato_gpu_multi_create(int num_gpus, const int* devices, erato_gpu_multi** out) {
+  if (!out) return fail(ERATO_GPU_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  const int ndev = erato_gpu_device_count();
+  if (ndev == 0) return fail(ERATO_GPU_E_NO_DEVICE, "no CUDA device visible");
+  if (num_gpus < 1 || num_gpus > 4096) return fail(ERATO_GPU_E_INVALID_ARG, "num_gpus out of range");
+  auto* m = new erato_gpu_multi();
+  m->num = num_gpus;
+  for (int g = 0; g < num_gpus; ++g) {
+    const int d = devices ? devices[g] : g;
+    if (d < 0 || d >= ndev) {
+      erato_gpu_multi_destroy(m);
+      return fail(ERATO_GPU_E_NO_DEVICE, "device " + std::to_string(d) + " not visible (" + std::to_string(ndev) +
+                                             " devices)");
+    }
+    m->devices.push_back(d);
+  }
+  m->ctx.assign(num_gpus, nullptr);
+  m->dcount.assign(num_gpus, nullptr);
+  for (int g = 0; g < num_gpus; ++g) {
+    int rc = erato_gpu_create(m->devices[g], &m->ctx[g]);
+    if (!rc && cudaSetDevice(m->devices[g]) == cudaSuccess &&
+        cudaMalloc(reinterpret_cast<void**>(&m->dcount[g]), 8) != cudaSuccess)
+      rc = fail(ERATO_GPU_E_CUDA, "count word allocation failed");
+    if (rc) {
+      const std::string msg = g_err;
+      erato_gpu_multi_destroy(m);
+      g_err = msg;
+      return rc;
+    }
+  }
+  std::vector<int> sorted = m->devices;
+  std::sort(sorted.begin(), sorted.end());
+  const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+  if (distinct) {  // NCCL communicators over the devices (one process, one comm per device)
+    const NcclApi& api = nccl();
+    if (!api.ok) {
+      erato_gpu_multi_destroy(m);
+      return fail(ERATO_GPU_E_CUDA, "NCCL unavailable: " + api.why);
+    }
+    m->comms.assign(num_gpus, nullptr);
+    const ncclResult_t r = api.CommInitAll(m->comms.data(), num_gpus, m->devices.data());
+    if (r != ncclSuccess) {
+      m->comms.clear();
+      erato_gpu_multi_destroy(m);
+      return fail(ERATO_GPU_E_CUDA, std::string("ncclCommInitAll: ") + api.GetErrorString(r));
+    }
+  }
+  *out = m;
+  return 0;
+}
+
+extern "C" int erato_gpu_multi_uses_nccl(const erato_gpu_multi* m) { return m && !m->comms.empty() ? 1 : 0; }
+
+namespace {
+// One shard per device thread: count-only (fd < 0) or streamed into fd.
+int multi_run(erato_gpu_multi* m, int fd, unsigned l, uint64_t f, uint64_t n, unsigned flags, uint64_t* count,
+              erato_gpu_stats* stats) {
+  int rc = erato_gpu_validate(l, f, n, flags, nullptr, nullptr);
+  if (rc) return rc;
+  const int G = m->num;
+  std::vector<int> rcs(G, 0);
+  std::vector<std::string> errs(G);
+  std::vector<erato_gpu_stats> st(G);
+  std::vector<uint64_t> parts(G, 0);
+  std::vector<std::thread> th;
+  for (int g = 0; g < G; ++g) {
+    th.emplace_back([&, g] {
+      uint64_t fg = 0, ng = 0;
+      erato_gpu_shard(f, n, g, G, &fg, &ng);
+      std::memset(&st[g], 0, sizeof(st[g]));
+      int r = 0;
+      erato_gpu_ctx* c = m->ctx[g];
+      if (cudaSetDevice(c->device) != cudaSuccess) r = fail(ERATO_GPU_E_CUDA, "cudaSetDevice");
+      if (!r && ng == 0) {  // empty shard (more devices than segments): count 0, still joins the reduction
+        r = cudaMemsetAsync(m->dcount[g], 0, 8, c->stream) == cudaSuccess ? 0 : fail(ERATO_GPU_E_CUDA, "memset");
+      } else if (!r && fd < 0) {
+        r = erato_gpu_run(c, l, fg, ng, flags, nullptr, m->dcount[g], nullptr, 1, &st[g]);
+      } else if (!r) {
+        r = write_shard(c, fd, l, f, fg, ng, flags, &st[g]);
+        if (!r && cudaMemcpyAsync(m->dcount[g], &st[g].prime_count, 8, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+          r = fail(ERATO_GPU_E_CUDA, "count upload");
+      }
+      if (!r && cudaStreamSynchronize(c->stream) != cudaSuccess) r = fail(ERATO_GPU_E_CUDA, "shard sync");
+      parts[g] = st[g].prime_count;
+      rcs[g] = r;
+      if (r) errs[g] = g_err;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int g = 0; g < G; ++g)
+    if (rcs[g]) {
+      g_err = errs[g];
+      return rcs[g];
+    }
+  uint64_t total = 0;
+  if (!m->comms.empty()) {
+    // the one collective: sum of the shards' device count words over NVLink
+    const NcclApi& api = nccl();
+    ncclResult_t r = api.GroupStart();
+    for (int g = 0; g < G && r == ncclSuccess; ++g) {
+      cudaSetDevice(m->devices[g]);
+      r = api.AllReduce(m->dcount[g], m->dcount[g], 1, ncclUint64, ncclSum, m->comms[g], m->ctx[g]->stream);
+    }
+    const ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(ERATO_GPU_E_CUDA, std::string("ncclAllReduce: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+    std::vector<uint64_t> red(G, 0);
+    for (int g = 0; g < G; ++g) {
+      CUDA_TRY(cudaSetDevice(m->devices[g]));
+      CUDA_TRY(cudaMemcpyAsync(&red[g], m->dcount[g], 8, cudaMemcpyDeviceToHost, m->ctx[g]->stream));
+      CUDA_TRY(cudaStreamSynchronize(m->ctx[g]->stream));
+    }
+    total = red[0];
+    for (int g = 1; g < G; ++g)
+      if (red[g] != total) return fail(ERATO_GPU_E_INVARIANT, "all-reduced counts differ across devices");
+  } else {
+    for (int g = 0; g < G; ++g) total += parts[g];
+  }
+  uint64_t check = 0;
+  for (int g = 0; g < G; ++g) check += parts[g];
+  if (check != total) return fail(ERATO_GPU_E_INVARIANT, "all-reduced count differs from the sum of the shards");
+  if (count) *count = total;
+  if (stats) {  // device times: max over shards (the shards run concurrently)
+    std::memset(stats, 0, sizeof(*stats));
+    stats->prime_count = total;
+    stats->segments = n;
+    for (int g = 0; g < G; ++g) {
+      stats->init_s = std::max(stats->init_s, st[g].init_s);
+      stats->small_s = std::max(stats->small_s, st[g].small_s);
+      stats->large_s = std::max(stats->large_s, st[g].large_s);
+      stats->total_s = std::max(stats->total_s, st[g].total_s);
+      stats->base_primes = std::max(stats->base_primes, st[g].base_primes);
+      stats->tiles += st[g].tiles;
+      stats->waves = std::max(stats->waves, st[g].waves);
+      stats->kernel_launches += st[g].kernel_launches;
+      stats->retries += st[g].retries;
+      stats->log_tile = std::max(stats->log_tile, st[g].log_tile);
+    }
+  }
+  return 0;
+}
+}  // namespace
+
+extern "C" int erato_gpu_multi_count(erato_gpu_multi* m, unsigned l, uint64_t f, uint64_t n, unsigned flags,
+                                     uint64_t* count, erato_gpu_stats* stats) {
+  if (!m) return fail(ERATO_GPU_E_INVALID_ARG, "multi is NULL");
+  return multi_run(m, -1, l, f, n, flags, count, stats);
+}
+
+extern "C" int erato_gpu_multi_write_table(erato_gpu_multi* m, const char* out_dir, unsigned l, uint64_t f,
+                                           uint64_t n, unsigned flags, char* path_out, size_t path_cap,
+                                           uint64_t* count, erato_gpu_stats* stats) {
+  if (!m || !out_dir) return fail(ERATO_GPU_E_INVALID_ARG, "NULL argument");
+  int rc = erato_gpu_validate(l, f, n, flags, nullptr, nullptr);
+  if (rc) return rc;
+  const std::string path = table_path(out_dir, l, f, n);
+  const std::string tmp = path + ".tmp." + std::to_string(::getpid());
+  const int fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) return fail(ERATO_GPU_IO_ERROR, "cannot open " + tmp);
+  rc = ::ftruncate(fd, (off_t)((n << l) / 8)) == 0 ? 0 : fail(ERATO_GPU_IO_ERROR, "truncate failed for " + tmp);
+  if (!rc) rc = multi_run(m, fd, l, f, n, flags, count, stats);  // shards pwrite concurrently
+  if (::close(fd) != 0 && !rc) rc = fail(ERATO_GPU_IO_ERROR, "close failed for " + tmp);
+  if (!rc && ::rename(tmp.c_str(), path.c_str()) != 0) rc = fail(ERATO_GPU_IO_ERROR, "rename to " + path + " failed");
+  if (rc) {
+    ::unlink(tmp.c_str());
+    return rc;
+  }
+  if (path_out && path_cap) std::snprintf(path_out, path_cap, "%s", path.c_str());
   return 0;
 }

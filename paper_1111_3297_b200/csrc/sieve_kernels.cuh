@@ -214,15 +214,23 @@ struct TileArgs {
   const uint32_t* hits;  // [gridDim.x][hcap] hit offsets (large primes), may be null
   uint32_t* hitcnt;      // [gridDim.x], zeroed after use
   uint32_t hcap;
-  uint32_t* table;               // output words (nullable: count only)
+  uint32_t* table;               // output words (nullable: count only); tile t writes at
+  uint64_t out_tile0;            //   table + (t - out_tile0) * S/32 (a wave slice when streaming)
   unsigned long long* count;     // zero-bit accumulator
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
+  unsigned long long* phase_ns;  // nullable: CTA 0 adds its pattern-phase time (masks_s)
 };
 
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 2048;  // medium primes below S/64 (pi(16384) = 1900 at S = 2^20)
 constexpr uint32_t kHitChunk = 256;        // hit records per warp chunk (1 KB of shared staging per warp)
 constexpr int kTileWarps = kTileThreads / 32;
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
 
@@ -298,6 +306,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   const uint64_t t64 = a.tile0 + blockIdx.x;
   const uint64_t tstart = t64 << log_s;
   const uint64_t g = a.g0 + tstart;
+  uint64_t t_start = 0;
+  if (a.phase_ns && blockIdx.x == 0 && tid == 0) t_start = globaltimer();
 
   {  // stage pattern tables and the wheel tables
     const uint4* src = reinterpret_cast<const uint4*>(a.ptab);
@@ -361,6 +371,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     }
   }
   __syncthreads();
+  if (a.phase_ns && blockIdx.x == 0 && tid == 0) atomicAdd(a.phase_ns, (unsigned long long)(globaltimer() - t_start));
   // the patterns also hit the primes 3..61 themselves: clear them if inside
   if (tid < 17) {
     const uint64_t idx = (c_small17[tid] - 1) / 2;
@@ -531,7 +542,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   const uint32_t valid = rem < S ? (uint32_t)rem : S;  // multiple of 16 except in the base sieve
   const uint32_t vbytes = (valid + 7) >> 3;  // the base sieve table may end inside a byte
   unsigned long long ones = 0;
-  uint32_t* out = a.table ? a.table + (tstart >> 5) : nullptr;
+  uint32_t* out = a.table ? a.table + (((t64 - a.out_tile0) << log_s) >> 5) : nullptr;
   for (uint32_t w4 = tid; w4 < (nw >> 2); w4 += bd) {
     const uint32_t w0 = w4 << 2;
     if (w0 * 32 >= valid) break;

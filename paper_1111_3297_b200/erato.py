@@ -211,13 +211,20 @@ class RunStats:
     gen_s: float = 0.0
     bin_s: float = 0.0
     large_records: int = 0
+    medium_primes: int = 0
+    ml_primes: int = 0
+    far_primes: int = 0
 
     @classmethod
     def _from(cls, s: _lib.Stats) -> "RunStats":
-        return cls(prime_count=s.prime_count, segments=s.segments, init_s=s.init_s, medium_s=s.small_s,
+        # masks_s: the pattern phase of the tile kernel (with PHASE_TIMING);
+        # medium_s: the rest of the tile kernel (medium primes, hit records, count)
+        return cls(prime_count=s.prime_count, segments=s.segments, init_s=s.init_s, masks_s=s.masks_s,
+                   medium_s=max(0.0, s.small_s - s.masks_s),
                    large_s=s.large_s, output_s=s.output_s, total_s=s.total_s, base_primes=s.base_primes,
                    tiles=s.tiles, log_tile=s.log_tile, waves=s.waves, kernel_launches=s.kernel_launches,
-                   retries=s.retries, gen_s=s.gen_s, bin_s=s.bin_s, large_records=s.large_records)
+                   retries=s.retries, gen_s=s.gen_s, bin_s=s.bin_s, large_records=s.large_records,
+                   medium_primes=s.medium_primes, ml_primes=s.ml_primes, far_primes=s.far_primes)
 
 
 @dataclass
@@ -288,14 +295,43 @@ class Context:
                                          C.c_void_p(stream or None), 1 if sync else 0, C.byref(st)))
         return RunStats._from(st)
 
-    def write_table(self, out_dir: str, params: SieveParams, part_f: int = 0, part_n: int = 0):
+    def write_table(self, out_dir: str, params: SieveParams, part_f: Optional[int] = None,
+                    part_n: Optional[int] = None):
+        """FileSink run.  part_f/part_n: one shard of params (erato_gpu_shard),
+        pwrite()n at its offset into the shared file; None = the whole table."""
+        if part_f is None or part_n is None:
+            part_f, part_n = params.f, params.n
         buf = C.create_string_buffer(4096)
         st = _lib.Stats()
         _check(_lib.load().erato_gpu_write_table(self._h, out_dir.encode(), params.l, params.f, params.n,
                                                  part_f, part_n, params.flags, buf, 4096, C.byref(st)))
         return buf.value.decode(), RunStats._from(st)
 
+    def stream(self, params: SieveParams, fn) -> RunStats:
+        """erato_gpu_run_to_sink: fn(view, offset) gets the table as ordered
+        contiguous byte slices (numpy views valid only during the call)."""
+        err = []
+
+        def cb(_user, ptr, offset, nbytes):
+            try:
+                fn(np.ctypeslib.as_array(ptr, shape=(nbytes,)), offset)
+                return 0
+            except BaseException as e:  # noqa: BLE001 — re-raised below
+                err.append(e)
+                return 1
+
+        cfn = _lib.SINK_FN(cb)
+        st = _lib.Stats()
+        rc = _lib.load().erato_gpu_run_to_sink(self._h, params.l, params.f, params.n, params.flags, cfn, None,
+                                               C.byref(st))
+        if err:
+            raise err[0]
+        _check(rc)
+        return RunStats._from(st)
+
     def extract_primes(self, params: SieveParams, cap: Optional[int] = None) -> np.ndarray:
+        """One sieve + device compaction; the first call (cap None) learns the
+        count, the second only copies the cached list (erato_gpu_extract_primes)."""
         L = _lib.load()
         cnt = C.c_uint64()
         if cap is None:
@@ -306,6 +342,50 @@ class Context:
         _check(L.erato_gpu_extract_primes(self._h, params.l, params.f, params.n, params.flags,
                                           out.ctypes.data_as(_lib.u64p), cap, C.byref(cnt)))
         return out[:min(cap, cnt.value)]
+
+
+class MultiGPU:
+    """erato_gpu_multi: contiguous range shards over several devices, one host
+    thread each, counts summed by one ncclAllReduce."""
+
+    def __init__(self, devices):
+        devices = list(devices)
+        L = _lib.load()
+        h = C.c_void_p()
+        arr = (C.c_int * len(devices))(*devices)
+        _check(L.erato_gpu_multi_create(len(devices), arr, C.byref(h)))
+        self._h = h
+        self.devices = devices
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(_lib.load().erato_gpu_multi_uses_nccl(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            _lib.load().erato_gpu_multi_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def count(self, params: SieveParams) -> RunStats:
+        st = _lib.Stats()
+        cnt = C.c_uint64()
+        _check(_lib.load().erato_gpu_multi_count(self._h, params.l, params.f, params.n, params.flags,
+                                                 C.byref(cnt), C.byref(st)))
+        return RunStats._from(st)
+
+    def write_table(self, out_dir: str, params: SieveParams):
+        buf = C.create_string_buffer(4096)
+        st = _lib.Stats()
+        cnt = C.c_uint64()
+        _check(_lib.load().erato_gpu_multi_write_table(self._h, out_dir.encode(), params.l, params.f, params.n,
+                                                       params.flags, buf, 4096, C.byref(cnt), C.byref(st)))
+        return buf.value.decode(), RunStats._from(st)
 
 
 _contexts: dict = {}
@@ -415,14 +495,27 @@ def run_sieve(params: SieveParams, sink: SegmentSink, opt: Optional[RunOptions] 
     elif isinstance(sink, FileSink):
         path, stats = ctx.write_table(sink.dir, params)
         sink._path = path
-    else:
+    elif isinstance(sink, TableSink):
         table, stats = ctx.table(params)
-        if isinstance(sink, TableSink):
-            sink._set_all(table)
-        else:
-            sb = params.segment_bytes()
-            for t in range(params.n):
-                sink.on_segment(table[t * sb:(t + 1) * sb], t, params)
+        sink._set_all(table)
+    else:
+        # any other sink: the table streams by (wave slices), re-cut into the
+        # reference's segments, handed over in order t = 0..n-1
+        sb = params.segment_bytes()
+        carry = bytearray()
+        nxt = [0]
+
+        def on_slice(view, offset):
+            carry.extend(view.tobytes())
+            while len(carry) >= sb:
+                seg = np.frombuffer(bytes(carry[:sb]), dtype=np.uint8)
+                del carry[:sb]
+                sink.on_segment(seg, nxt[0], params)
+                nxt[0] += 1
+
+        stats = ctx.stream(params, on_slice)
+        if nxt[0] != params.n or carry:
+            raise Error(errc.io_error, f"streamed {nxt[0]} of {params.n} segments")
     sink.finish(params)
     stats.segments = params.n
     return stats

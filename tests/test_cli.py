@@ -57,3 +57,23 @@ def test_cli_smoke_contract(cli):
         csv = os.path.join(d, "b.csv")
         r = run(cli, "bench", "--exps", "12,13", "--csv", csv, "--reps", "2")
         assert r.returncode == 0 and open(csv).read().startswith("e,seconds,l\n")
+
+
+@pytest.mark.gpu
+def test_cli_multi_gpu_shards(cli):
+    """--devices: range shards driven by the C-ABI multi-GPU entry (here all on
+    device 0, the 1-GPU box's test topology); count and file as one GPU."""
+    r = run(cli, "sieve", "--log-seg", "20", "--first", "523776", "--segments", "1024", "--count-only",
+            "--devices", "0,0")
+    assert r.returncode == 0 and "primes    77449842" in r.stdout, r.stderr
+    with tempfile.TemporaryDirectory() as d:
+        r = run(cli, "sieve", "--log-seg", "10", "--first", "2048", "--segments", "4", "--out-dir", d,
+                "--devices", "0,0,0")
+        assert r.returncode == 0 and "primes    542" in r.stdout, r.stderr
+        assert os.path.getsize(os.path.join(d, "erato_l10_f2048_n4.bits")) == 512
+    r = run(cli, "sieve", "--log-seg", "20", "--first", "523776", "--segments", "1024", "--count-only",
+            "--gpus", "1")
+    assert r.returncode == 0 and "primes    77449842" in r.stdout
+    r = run(cli, "sieve", "--log-seg", "20", "--first", "523776", "--segments", "16", "--count-only",
+            "--devices", "0,99")
+    assert r.returncode == 2 and "NO_DEVICE" in r.stderr

@@ -1,7 +1,8 @@
-"""World-size-2 gloo test of the N>1 path on CPU: contiguous shards, one
-count all-reduce, shard tables concatenating to the full table.  The
+"""World-size-2 and -4 gloo tests of the N>1 path on CPU: contiguous shards,
+one count all-reduce, shard tables concatenating to the full table, and a
+rank with an empty shard (world > n) that still joins the reduction.  The
 per-rank sieve is the CPU oracle here (test infrastructure); on the B200 box
-it is erato_gpu_run (bench.py)."""
+it is the CUDA path (tests/test_gpu_output_multi.py, bench.py)."""
 import os
 import socket
 
@@ -11,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 CASES = [(12, 4096, 37, False, False), (17, 0, 64, False, True), (20, (1 << 19) - 512, 16, False, False),
-         (10, 6, 3, False, False)]
+         (10, 6, 3, False, False), (12, 4096, 3, False, False)]  # the last: world 4 > n = 3 (an empty shard)
 
 
 def _free_port():
@@ -41,13 +42,14 @@ def _worker(rank, world, port, q):
         res = run_sharded(l, f, n, sieve_count, rank, world, torch_allreduce_sum(), test_mode=tm,
                           allow_overlap=ovl)
         gathered = [None] * world
-        dist.all_gather_object(gathered, (res.params.f, res.params.n, tables.get("t", np.zeros(0, np.uint8))))
+        fg, ng = (res.params.f, res.params.n) if res.params is not None else (f + n, 0)
+        dist.all_gather_object(gathered, (fg, ng, tables.get("t", np.zeros(0, np.uint8))))
         out.append((res.total, gathered))
     q.put((rank, out))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_gloo_shards_concatenate_and_counts_sum(world, restated):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -63,6 +65,6 @@ def test_gloo_shards_concatenate_and_counts_sum(world, restated):
         full, cfull = restated.bit_table(l, f, n, test_mode=tm, allow_overlap=ovl)
         totals = {results[r][k][0] for r in range(world)}
         assert totals == {cfull}
-        parts = results[0][k][1]
+        parts = [x for x in results[0][k][1] if x[1]]
         assert parts[0][0] == f and sum(x[1] for x in parts) == n
         assert np.array_equal(np.concatenate([x[2] for x in parts]), full)

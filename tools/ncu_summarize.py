@@ -63,7 +63,38 @@ def full_report(path: str) -> str:
     return "\n".join(out)
 
 
+def traffic_json(path: str, config: int, out: str) -> dict:
+    """profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum
+    per launch of each wave kernel (mean over the captured launches), tagged
+    with the hash of the kernel sources bench.py compares before using it."""
+    import json
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import kernel_src_sha
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h = rows[0]
+    unit = rows[1]
+    acc = collections.defaultdict(list)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for row in rows[2:]:
+        d = dict(zip(h, row))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("eg::", "").split("<")[0]
+        b = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(d[k].replace(",", "")) * scale.get(unit[h.index(k)], 1)
+        acc[name].append(b)
+    res = {"kernel_src_sha": kernel_src_sha(), "config": config, "source": os.path.basename(path),
+           "per_launch_bytes": {k: round(sum(v) / len(v)) for k, v in acc.items()}}
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1)
+    return res
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "--traffic":
+        print(traffic_json(sys.argv[2], int(sys.argv[3]), sys.argv[4]))
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(full_report(p) if p.endswith(".ncu-rep") else launch_list(p))
         print()
