@@ -69,7 +69,7 @@ METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roo
 # mix), 1024-thread CTAs over a 128 KiB tile: microbench/mb_atomics.cu
 # k_smem_atom_pure (16 unrolled ATOMS per loop, addresses in registers),
 # profiles/r02_microbench_atomics.log
-R_ATOM_MEASURED = 3.47e12
+R_ATOM_MEASURED = 4.06e12
 NCU_TRAFFIC_FILE = os.path.join(HERE, "profiles", "ncu_traffic.json")
 KERNEL_SOURCES = [os.path.join(HERE, "paper_1111_3297_b200", "csrc", x) for x in ("sieve_kernels.cuh", "erato_gpu.cu")]
 

@@ -45,6 +45,9 @@ def build(reference: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
     if reference and os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-s", "-j8", "-C", HERE, "all"], check=True)
+        # the INTEGRATION.md binding test (needs liberato_gpu.so built first)
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1111_3297_b200", "liberato_gpu.so")):
+            subprocess.run(["make", "-s", "-C", HERE, "binding"], check=True)
 
 
 def _ptr(a: np.ndarray, t):

@@ -233,6 +233,11 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 __device__ __forceinline__ void mark(uint32_t* tile, uint32_t q) { atomicOr(&tile[q >> 5], 1u << (q & 31)); }
+// the same on a 32-bit shared address (the tile sits at the start of the
+// dynamic shared memory): SHF + LOP3 + SHF.L.W + ATOMS [R + UR] per mark
+__device__ __forceinline__ void mark_a(uint32_t tile_a, uint32_t q) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tile_a + ((q >> 5) << 2)), "r"(1u << (q & 31)) : "memory");
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" : : "r"(dst), "l"(src) : "memory");
@@ -292,9 +297,9 @@ __device__ __forceinline__ uint32_t med_first(const uint4 rec, uint32_t t, float
 template <bool P2, bool HITS>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   extern __shared__ uint4 smem4[];
-  uint32_t* const pat = reinterpret_cast<uint32_t*>(smem4);
-  uint32_t* const tile = pat + kPatWords;
-  uint2* const s_wq = reinterpret_cast<uint2*>(tile + ((1u << a.log_s) >> 5));  // [nmed_warp] (q0, p | s<<29)
+  uint32_t* const tile = reinterpret_cast<uint32_t*>(smem4);  // first: mark addresses need no base add
+  uint32_t* const pat = tile + ((1u << a.log_s) >> 5);
+  uint2* const s_wq = reinterpret_cast<uint2*>(pat + kPatWords);  // [nmed_warp] (q0, p | s<<29)
   uint4* const s_hits = reinterpret_cast<uint4*>(s_wq + ((a.nmed_warp + 1) & ~1u));  // [warps][kHitChunk/4] if hits
   __shared__ unsigned long long s_red[kTileWarps];
   __shared__ uint8_t s_combo[64];  // [c'] = adv | cls << 3 (c' = 0..30); [32 + r] = cls of r
@@ -311,7 +316,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
 
   {  // stage pattern tables and the wheel tables
     const uint4* src = reinterpret_cast<const uint4*>(a.ptab);
-    for (uint32_t i = tid; i < kPatWords / 4; i += bd) smem4[i] = src[i];
+    uint4* const pat4 = reinterpret_cast<uint4*>(pat);
+    for (uint32_t i = tid; i < kPatWords / 4; i += bd) pat4[i] = src[i];
     if (tid < 31) {
       const uint32_t r = tid % 30u;
       s_combo[tid] = (uint8_t)(c_adv[r] | (c_cls[r + c_adv[r]] << 3));
@@ -330,6 +336,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   const uint32_t t = (uint32_t)(t64 - a.tbase);  // tile index within the chunk (< 2^20)
   const float tf = __uint2float_rz(t);
   const uint32_t combo_a = smem_addr(s_combo);
+  const uint32_t tile_a = smem_addr(tile);
   // 0. start offsets of the group-marked medium primes (p < S/64), lane-
   // parallel into shared memory (no barrier of its own: phase 1's covers it)
   for (uint32_t i = tid; i < a.nmed_warp; i += bd) {
@@ -417,17 +424,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         const uint4 v0 = s_hits[warp * (kHitChunk / 4) + lane], v1 = s_hits[warp * (kHitChunk / 4) + 32 + lane];
         const uint32_t i0 = ch * kHitChunk + 4 * lane, i1 = i0 + 128;
         if (i1 + 3 < hcnt) {
-          mark(tile, v0.x); mark(tile, v0.y); mark(tile, v0.z); mark(tile, v0.w);
-          mark(tile, v1.x); mark(tile, v1.y); mark(tile, v1.z); mark(tile, v1.w);
+          mark_a(tile_a, v0.x); mark_a(tile_a, v0.y); mark_a(tile_a, v0.z); mark_a(tile_a, v0.w);
+          mark_a(tile_a, v1.x); mark_a(tile_a, v1.y); mark_a(tile_a, v1.z); mark_a(tile_a, v1.w);
         } else {
-          if (i0 < hcnt) mark(tile, v0.x);
-          if (i0 + 1 < hcnt) mark(tile, v0.y);
-          if (i0 + 2 < hcnt) mark(tile, v0.z);
-          if (i0 + 3 < hcnt) mark(tile, v0.w);
-          if (i1 < hcnt) mark(tile, v1.x);
-          if (i1 + 1 < hcnt) mark(tile, v1.y);
-          if (i1 + 2 < hcnt) mark(tile, v1.z);
-          if (i1 + 3 < hcnt) mark(tile, v1.w);
+          if (i0 < hcnt) mark_a(tile_a, v0.x);
+          if (i0 + 1 < hcnt) mark_a(tile_a, v0.y);
+          if (i0 + 2 < hcnt) mark_a(tile_a, v0.z);
+          if (i0 + 3 < hcnt) mark_a(tile_a, v0.w);
+          if (i1 < hcnt) mark_a(tile_a, v1.x);
+          if (i1 + 1 < hcnt) mark_a(tile_a, v1.y);
+          if (i1 + 2 < hcnt) mark_a(tile_a, v1.z);
+          if (i1 + 3 < hcnt) mark_a(tile_a, v1.w);
         }
         __syncwarp();  // every lane has read its staging before it is refilled
         pend = false;
@@ -466,12 +473,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       uint32_t q = idx < lim ? w.x + p * (nib(s_cum[s], j & 7) + 15u * (j >> 3)) : S;
       const uint32_t step = (15u * p) << shp;
       for (; q + 3 * step < S; q += 4 * step) {
-        mark(tile, q);
-        mark(tile, q + step);
-        mark(tile, q + 2 * step);
-        mark(tile, q + 3 * step);
+        mark_a(tile_a, q);
+        mark_a(tile_a, q + step);
+        mark_a(tile_a, q + 2 * step);
+        mark_a(tile_a, q + 3 * step);
       }
-      for (; q < S; q += step) mark(tile, q);
+      for (; q < S; q += step) mark_a(tile_a, q);
       if (HITS && ++since >= every) {
         since = 0;
         consume();
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         if ((p << 3) > S) {
           uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
           while (q < S) {
-            mark(tile, q);
+            mark_a(tile_a, q);
             q += (dd & 15u) * p;
             dd = __funnelshift_r(dd, dd, 4);
           }
@@ -505,19 +512,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
                          o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
           const uint32_t per = 15u * p;
           for (; q + o7 < S; q += per) {
-            mark(tile, q);
-            mark(tile, q + o1);
-            mark(tile, q + o2);
-            mark(tile, q + o3);
-            mark(tile, q + o4);
-            mark(tile, q + o5);
-            mark(tile, q + o6);
-            mark(tile, q + o7);
+            mark_a(tile_a, q);
+            mark_a(tile_a, q + o1);
+            mark_a(tile_a, q + o2);
+            mark_a(tile_a, q + o3);
+            mark_a(tile_a, q + o4);
+            mark_a(tile_a, q + o5);
+            mark_a(tile_a, q + o6);
+            mark_a(tile_a, q + o7);
           }
           // last partial period: a short wheel walk from class s
           uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
           while (q < S) {
-            mark(tile, q);
+            mark_a(tile_a, q);
             q += (dd & 15u) * p;
             dd = __funnelshift_r(dd, dd, 4);
           }
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
   for (uint32_t w4 = tid; w4 < (nw >> 2); w4 += bd) {
     const uint32_t w0 = w4 << 2;
     if (w0 * 32 >= valid) break;
-    uint4 v = smem4[kPatWords / 4 + w4];
+    uint4 v = smem4[w4];
     if ((w0 + 4) * 32 > valid) {  // partial quad at the end of the run
       uint32_t e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
