@@ -272,10 +272,10 @@ int create_impl(erato_gpu_ctx* c) {
                                         eg::kTileWarps * eg::kHitChunk * 4)));
   CUDA_TRY(cudaFuncSetAttribute(eg::k_bin, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(eg::BinSmem)));
-  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_ml, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(eg::MlSmem)));
-  CUDA_TRY(cudaFuncSetAttribute(eg::k_scatter_far, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(eg::FarSmem)));
+  for (auto km : {eg::k_scatter_ml<false>, eg::k_scatter_ml<true>})
+    CUDA_TRY(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::MlSmem)));
+  for (auto kf : {eg::k_scatter_far<false>, eg::k_scatter_far<true>})
+    CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::FarSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure((8192 + eg::kMedPad) * 16));
@@ -636,6 +636,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     ++launches;
     const bool have_large = nml + nfar > 0;
     uint32_t ring = 1, bcap = 1, hcap = 4, rcap = 1, fcap = 1;
+    bool split = false, far7 = false, ml7 = false;
     if (have_large) {
       const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
       const double sum_recip = std::max(0.0, std::log(lnP / std::log((double)P.S))) + 0.02;  // sum 1/p, S<p<=P
@@ -648,7 +649,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       CUDA_TRY(c->hitcnt.ensure((uint64_t)P.MW * P.W * 4));
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.MW * P.W * 4, st));
       if (nfar) {
-        ring = (uint32_t)std::min<uint64_t>(4ull * pmax / P.WS + 3, P.nwaves + 2);
+        // an entry's next hit lies at most 3p (mod 30) or 5p (mod 210: two wheel steps) ahead
+        ring = (uint32_t)std::min<uint64_t>(6ull * pmax / P.WS + 3, P.nwaves + 2);
         if (ring > (uint32_t)eg::kMaxRing) return fail(ERATO_GPU_RANGE_TOO_LARGE, "far bucket ring exceeds 256 waves");
         const double sr_far = std::max(0.0, std::log(lnP / std::log((double)P.MW * P.WS))) + 0.01;
         const double eb = (double)P.WS * (8.0 / 15.0) * sr_far;
@@ -667,6 +669,23 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         CUDA_TRY(c->fslot.ensure(gen_warps * fcap));
         CUDA_TRY(c->fcount.ensure(gen_warps * 4));
       }
+      // large-prime path: k_scatter_ml + k_scatter_far (default), or k_gen +
+      // k_bin (ERATO_GPU_SCATTER=genbin, or when a wave has more than 256 tiles
+      // or ring slots, or 32-bit list offsets do not fit)
+      const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
+      const bool sortable = ring <= (uint32_t)eg::kScBins && (uint64_t)P.MW * P.W <= (uint64_t)eg::kScBins;
+      const bool idx32 = (uint64_t)P.MW * P.W * hcap + eg::kScTrash < (1ull << 32) &&
+                         (uint64_t)ring * bcap + eg::kScTrash < (1ull << 32);
+      split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
+      // far primes skip cofactors divisible by 7 (mod-210 entries) when p < 2^31 and q < 2^28 fit
+      const char* f7_env = std::getenv("ERATO_GPU_FAR7");
+      far7 = split && nfar && pmax < (1u << 31) && P.WS <= (1u << 28) && !(f7_env && std::strcmp(f7_env, "0") == 0);
+      // ML primes too (p < 2^28 and next-hit offsets < 6p < 2^30 need WS <= 170 * 2^20), when they all
+      // hit a wave >= ~4 times (p <= WS/8: cfg4 -7% ML time); with primes up to WS (cfg5) the extra
+      // data-dependent step in the walk costs more than the skipped records save (+13% measured)
+      const char* m7_env = std::getenv("ERATO_GPU_ML7");
+      ml7 = split && nml && P.MW == 1 && P.WS <= 170u * (1u << 20) &&
+            (m7_env ? std::strcmp(m7_env, "1") == 0 : idense >= iWS);
       CUDA_TRY(c->bcount.ensure((uint64_t)ring * 4 + 4));
       CUDA_TRY(cudaMemsetAsync(c->bcount.p, 0, (uint64_t)ring * 4 + 4, st));
       CUDA_TRY(cudaMemsetAsync(d_scal + 17, 0, 8, st));  // overflow flag
@@ -686,6 +705,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       sa.inv_ws = 1.0 / (double)P.WS;
       sa.overflow = reinterpret_cast<int*>(d_scal + 17);
       if (const char* inj = std::getenv("ERATO_GPU_TEST_INJECT")) sa.inject = std::atoi(inj);  // tests only
+      sa.far7 = far7 ? 1 : 0;
+      sa.ml7 = ml7 ? 1 : 0;
       const uint64_t nl = nprimes - iS;
       eg::k_setup_large<<<(unsigned)((nl + eg::kSetupThreads - 1) / eg::kSetupThreads), eg::kSetupThreads, 0, st>>>(sa);
       ++launches;
@@ -694,7 +715,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         const unsigned __int128 x_hi = (unsigned __int128)P.u + 2 * (unsigned __int128)(P.ntiles << P.log_s) - 2;
         const uint64_t xh = x_hi > UINT64_MAX ? UINT64_MAX : (uint64_t)x_hi;
         eg::k_expected_records<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(
-            c->primes.as<uint32_t>(), iS, nprimes, P.u, xh, reinterpret_cast<unsigned long long*>(d_scal + 19));
+            c->primes.as<uint32_t>(), iS, nprimes, P.u, xh, reinterpret_cast<unsigned long long*>(d_scal + 19),
+            ml7 ? iS : (far7 ? iWS : nprimes), far7 ? nprimes : iWS);
         ++launches;
       }
     } else {
@@ -787,25 +809,17 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
-    // large-prime path: k_scatter_ml + k_scatter_far (default), or k_gen +
-    // k_bin (ERATO_GPU_SCATTER=genbin, or when a wave has more than 256 tiles
-    // or ring slots, or 32-bit list offsets do not fit)
-    const char* sc_env = std::getenv("ERATO_GPU_SCATTER");
-    const bool sortable = ring <= (uint32_t)eg::kScBins && (uint64_t)P.MW * P.W <= (uint64_t)eg::kScBins;
-    const bool idx32 = (uint64_t)P.MW * P.W * hcap + eg::kScTrash < (1ull << 32) &&
-                       (uint64_t)ring * bcap + eg::kScTrash < (1ull << 32);
-    const bool split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
     eg::ScatterArgs sca{};
     uint32_t ml_blocks = c->nsm, far_blocks = c->nsm;
     if (split) {
       int occ = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml, eg::kMlWarps * 32,
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml<false>, eg::kMlWarps * 32,
                                                              sizeof(eg::MlSmem)));
       // no more CTAs than units of work (small runs: a handful of ML primes)
       const uint64_t ml_units = (nml + 31) / 32;
       ml_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
                                                std::max<uint64_t>(1, (ml_units + eg::kMlWarps - 1) / eg::kMlWarps));
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_far, eg::kFarWarps * 32,
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_far<false>, eg::kFarWarps * 32,
                                                              sizeof(eg::FarSmem)));
       const uint64_t far_units = (std::min<uint64_t>(nfar, bcap) + 31) / 32;  // bucket size bound
       far_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
@@ -859,7 +873,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             m.WS = P.MW * P.WS;
             m.hits = c->hits.as<uint32_t>();
             m.hitcnt = c->hitcnt.as<uint32_t>();
-            eg::k_scatter_ml<<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(m);
+            if (ml7) eg::k_scatter_ml<true><<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(m);
+            else eg::k_scatter_ml<false><<<ml_blocks, eg::kMlWarps * 32, sizeof(eg::MlSmem), st>>>(m);
             launches += 1;
           }
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
@@ -871,7 +886,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             sca.far_in_count = ga.far_in_count;
             sca.hits = hits_w;
             sca.hitcnt = hitcnt_w;
-            eg::k_scatter_far<<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
+            if (far7) eg::k_scatter_far<true><<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
+            else eg::k_scatter_far<false><<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
             launches += 1;
           }
         } else {
@@ -892,7 +908,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         if (flags & ERATO_GPU_CHECK_INVARIANTS) {
           eg::k_check_wave<<<(unsigned)c->nsm, 256, 0, st>>>(
               hitcnt_w, ntw, hcap, nfar ? ga.far_in : nullptr, ga.far_in_count, bcap, P.WS,
-              reinterpret_cast<unsigned long long*>(d_scal + 18), reinterpret_cast<int*>(d_scal + 21));
+              reinterpret_cast<unsigned long long*>(d_scal + 18), reinterpret_cast<int*>(d_scal + 21), far7 ? 1 : 0);
           ++launches;
         }
       }

@@ -94,7 +94,8 @@ __device__ __forceinline__ uint32_t mod30_u64(uint64_t c) {
 // (src/wheel.cpp:43-47) plus wheel_align (src/wheel.cpp:60-69) for 64-bit
 // starts: floor(x/p) from an fp64 estimate (off by at most one), then the
 // exact remainder in wrap-around u64 arithmetic.
-__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint32_t& s) {
+__device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint32_t& s,
+                                              uint64_t* cof = nullptr) {
   uint64_t c = __double2ull_rz(__dmul_rz(__ull2double_rz(x), __drcp_rn((double)p)));
   int64_t r = (int64_t)(x - c * p);  // true remainder, in (-p, 2p)
   if (r < 0) {
@@ -117,7 +118,26 @@ __device__ __forceinline__ uint64_t first_hit(uint32_t p, uint64_t x, uint64_t c
   const uint32_t a = c_adv[cm];
   s = c_cls[cm + a];
   d += (uint64_t)a * p;
+  if (cof) *cof = c + a;  // the cofactor of the returned hit
   return d >> 1;
+}
+
+// Far entries (u64).  Mod-30 format: p | (q | s << 29) << 32.  Mod-210 format
+// (FAR7, when every far prime is < 2^31 and a wave spans <= 2^28 bits): the
+// entry also carries the cofactor mod 7, and a far prime skips its multiples
+// whose cofactor is divisible by 7 (those are marked by the pattern of 7):
+//   bits 0..29 (p-1)/2 | bits 30..57 q | bits 58..60 s | bits 61..63 c mod 7 (1..6)
+__device__ __forceinline__ uint64_t far7_pack(uint32_t p, uint32_t q, uint32_t s, uint32_t c7) {
+  return (uint64_t)(p >> 1) | ((uint64_t)q << 30) | ((uint64_t)(s & 7) << 58) | ((uint64_t)c7 << 61);
+}
+// ML states (uint2).  Mod-30: {p | s << 29, pos}.  Mod-210 (ML7, when a wave
+// spans at most 170 * 2^20 bits, so p < 2^28 and pos < 6p < 2^30):
+//   x = p | s << 28 | (c7 & 1) << 31,   y = pos | (c7 >> 1) << 30.
+__device__ __forceinline__ uint2 ml7_pack(uint32_t p, uint32_t pos, uint32_t s, uint32_t c7) {
+  return make_uint2(p | ((s & 7) << 28) | ((c7 & 1) << 31), pos | ((c7 >> 1) << 30));
+}
+__device__ __forceinline__ uint32_t far_q(uint64_t e, bool far7) {
+  return far7 ? (uint32_t)(e >> 30) & 0xfffffffu : (uint32_t)(e >> 32) & 0x1fffffffu;
 }
 
 // ---------------------------------------------------------------------------
@@ -1250,6 +1270,7 @@ constexpr uint32_t kScTrash = (uint32_t)(MlSmem::R * kMlWarps > FarSmem::R * kFa
 
 __device__ __forceinline__ uint32_t rotr4(uint32_t x) { return __funnelshift_r(x, x, 4); }
 
+template <bool ML7>
 __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, uint32_t nblk, MlSmem& sm) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t t = tid; t < kScBins; t += blockDim.x) sm.cnt[t] = 0;
@@ -1267,7 +1288,20 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nml;
   uint2 e0 = ok ? a.ml[idx] : make_uint2(0, 0);
-  uint32_t p = e0.x & 0x1fffffffu, pos = ok ? e0.y : B, s = e0.x >> 29;
+  uint32_t p, pos, s, c7 = 0;
+  auto decode = [&](uint2 e) {
+    if (ML7) {
+      p = e.x & 0x0fffffffu;
+      s = (e.x >> 28) & 7;
+      c7 = (e.x >> 31) | ((e.y >> 30) << 1);
+      pos = ok ? e.y & 0x3fffffffu : B;
+    } else {
+      p = e.x & 0x1fffffffu;
+      s = e.x >> 29;
+      pos = ok ? e.y : B;
+    }
+  };
+  decode(e0);
   uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
   // the next kMlPf units' primes and states are in flight (a sparse unit
   // takes only a few steps, far less than a DRAM round trip)
@@ -1286,7 +1320,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
     while (live && k < (uint32_t)kMlSteps) {
       const bool v = pos < B;
       if (!__any_sync(kFull, v)) {
-        if (ok) a.ml[idx] = make_uint2(p | ((s & 7) << 29), pos - WS);
+        if (ok) a.ml[idx] = ML7 ? ml7_pack(p, pos - WS, s, c7) : make_uint2(p | ((s & 7) << 29), pos - WS);
         u += nw;
         if (u >= nu) {
           live = false;
@@ -1294,9 +1328,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
         }
         idx = u * 32 + lane;
         ok = idx < a.nml;
-        p = pf[0].x & 0x1fffffffu;
-        pos = ok ? pf[0].y : B;
-        s = pf[0].x >> 29;
+        decode(pf[0]);
         dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
 #pragma unroll
         for (int k = 0; k + 1 < kMlPf; ++k) pf[k] = pf[k + 1];
@@ -1310,9 +1342,21 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
       rk_val = r;
       ++k;
       if (v) {
-        pos += (dd & 15u) * p;
+        const uint32_t D = dd & 15u;
+        pos += D * p;
         dd = rotr4(dd);
         ++s;
+        if (ML7) {  // the next admissible cofactor may be divisible by 7: then take the one after
+          c7 += 2 * D;
+          c7 -= c7 >= 7 ? 7 : 0;
+          if (c7 == 0) {
+            const uint32_t D2 = dd & 15u;
+            pos += D2 * p;
+            dd = rotr4(dd);
+            ++s;
+            c7 = 2 * D2;
+          }
+        }
       }
     }
     if (rk_pend) st_rank(rk_addr, rk_val);
@@ -1323,6 +1367,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   }
 }
 
+template <bool FAR7>
 __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, uint32_t nblk, FarSmem& sm) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (uint32_t t = tid; t < kScBins; t += blockDim.x) {
@@ -1362,7 +1407,17 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
       for (int j = 0; j + 1 < kFarPf; ++j) pfe[j] = pfe[j + 1];
       pfe[kFarPf - 1] = load(u + kFarPf * nw);
       u += nw;
-      const uint32_t p = (uint32_t)e, q = (uint32_t)(e >> 32) & 0x1fffffffu, s = (uint32_t)(e >> 61);
+      uint32_t p, q, s, c7 = 0;
+      if (FAR7) {
+        p = 2 * ((uint32_t)e & 0x3fffffffu) + 1;
+        q = (uint32_t)(e >> 30) & 0xfffffffu;
+        s = (uint32_t)(e >> 58) & 7;
+        c7 = (uint32_t)(e >> 61);
+      } else {
+        p = (uint32_t)e;
+        q = (uint32_t)(e >> 32) & 0x1fffffffu;
+        s = (uint32_t)(e >> 61);
+      }
       const bool emit = ok && q < lim;
       const uint32_t r1 = stage_rec(emit ? cnt_a + ((q >> shift) << 2) : sink_a, reg_a + (k << 7), emit ? q : kNoRec);
       if (k) {  // ranks of the previous step
@@ -1372,8 +1427,18 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
       rk1 = r1;
       // next hit q + D*p lies d waves ahead (Lemma 2): fp32 estimate of d,
       // then the exact remainder in 32-bit wrap-around arithmetic
-      const uint32_t D = wheel_D(s);
-      // (q + D*p < 2^29 + 3*2^32: the fp32 estimate is off by at most one wave)
+      uint32_t D = wheel_D(s), s1 = s + 1;
+      if (FAR7) {  // the next admissible cofactor may be divisible by 7: then take the one after
+        c7 += 2 * D;
+        c7 -= c7 >= 7 ? 7 : 0;
+        if (c7 == 0) {
+          const uint32_t D2 = wheel_D(s1 & 7);
+          D += D2;
+          c7 = 2 * D2;
+          ++s1;
+        }
+      }
+      // (q + D*p < 2^29 + 5*2^32: the fp32 estimate is off by at most one wave)
       uint32_t d = __float2uint_rz(__fmaf_rn((float)D, (float)p, (float)q) * a.inv_ws_f);
       int32_t r = (int32_t)(q + D * p - d * WS);
       const bool lo = r < 0;
@@ -1385,8 +1450,10 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
       const bool keep = ok && d < left;
       uint32_t slot = a.wslot + d;
       if (slot >= ring) slot -= ring;
-      rk2 = stage_far(keep ? fcnt_a + (slot << 2) : fsink_a, ent_a + (k << 8), slot_a + (k << 5),
-                      (uint64_t)p | ((uint64_t)((uint32_t)r | (((s + 1) & 7) << 29)) << 32), keep ? slot : kNoSlot);
+      const uint64_t ne = FAR7 ? far7_pack(p, (uint32_t)r, s1, c7)
+                               : (uint64_t)p | ((uint64_t)((uint32_t)r | ((s1 & 7) << 29)) << 32);
+      rk2 = stage_far(keep ? fcnt_a + (slot << 2) : fsink_a, ent_a + (k << 8), slot_a + (k << 5), ne,
+                      keep ? slot : kNoSlot);
     }
     if (k) {
       st_rank(rank_a + ((k - 1) << 6), rk1);
@@ -1401,20 +1468,22 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
 #ifndef EG_ML_MINB
 #define EG_ML_MINB 0
 #endif
+template <bool ML7>
 #if EG_ML_MINB
 __global__ void __launch_bounds__(kMlWarps * 32, EG_ML_MINB) k_scatter_ml(const ScatterArgs a) {
 #else
 __global__ void __launch_bounds__(kMlWarps * 32) k_scatter_ml(const ScatterArgs a) {
 #endif
   extern __shared__ uint4 smem_raw[];
-  scatter_ml(a, blockIdx.x, gridDim.x, *reinterpret_cast<MlSmem*>(smem_raw));
+  scatter_ml<ML7>(a, blockIdx.x, gridDim.x, *reinterpret_cast<MlSmem*>(smem_raw));
 }
 #ifndef EG_FAR_MINB
 #define EG_FAR_MINB 6  // 40 registers: 6 CTAs per SM (the shared-memory limit); 48 measured 3% slower
 #endif
+template <bool FAR7>
 __global__ void __launch_bounds__(kFarWarps * 32, EG_FAR_MINB) k_scatter_far(const ScatterArgs a) {
   extern __shared__ uint4 smem_raw[];
-  scatter_far(a, blockIdx.x, gridDim.x, *reinterpret_cast<FarSmem*>(smem_raw));
+  scatter_far<FAR7>(a, blockIdx.x, gridDim.x, *reinterpret_cast<FarSmem*>(smem_raw));
 }
 
 // ---------------------------------------------------------------------------
@@ -1569,6 +1638,8 @@ struct SetupArgs {
   double inv_ws;
   int* overflow;
   int inject;  // test-only fault injection on the first far prime: 1 drop its entry, 2 corrupt its q
+  int far7;    // far entries in the mod-210 format (far7_pack)
+  int ml7;     // ML states in the mod-210 format (ml7_pack)
 };
 
 constexpr int kSetupThreads = 1024;
@@ -1586,10 +1657,32 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     uint32_t s;
     // cofactor >= 2 (-> >= 7 after the wheel): never marks p itself and
     // keeps the first hit within 3.5p of the interval start in overlap runs
-    const uint64_t pos = first_hit(p, a.x0, 2, s);
+    uint64_t cof = 0;
+    uint64_t pos = first_hit(p, a.x0, 2, s, &cof);
     if (i < a.i_ml_end) {
-      a.ml[i - a.i0] = make_uint2(p | (s << 29), (uint32_t)pos);
+      if (a.ml7) {  // skip a first hit whose cofactor 7 divides (the next one cannot)
+        uint32_t c7 = (uint32_t)(cof % 7);
+        if (c7 == 0) {
+          const uint32_t D = wheel_D(s);
+          pos += (uint64_t)D * p;
+          c7 = 2 * D;
+          s = (s + 1) & 7;
+        }
+        a.ml[i - a.i0] = ml7_pack(p, (uint32_t)pos, s, c7);
+      } else {
+        a.ml[i - a.i0] = make_uint2(p | (s << 29), (uint32_t)pos);
+      }
     } else {
+      uint32_t c7 = 0;
+      if (a.far7) {  // cofactor mod 7 of the first hit; skip it if 7 divides it (the next one cannot)
+        c7 = (uint32_t)(cof % 7);
+        if (c7 == 0) {
+          const uint32_t D = wheel_D(s);
+          pos += (uint64_t)D * p;
+          c7 = 2 * D;
+          s = (s + 1) & 7;
+        }
+      }
       // d = pos / WS: fp64 estimate (pos < 2^40, off by at most one), exact fix
       uint64_t d = __double2ull_rz(__dmul_rz(__ull2double_rz(pos), a.inv_ws));
       if (d * a.WS > pos) --d;
@@ -1597,10 +1690,11 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
       if (d < a.nwaves) {
         app = true;
         slotb = (uint32_t)d % a.ring;
-        ne = (uint64_t)p | ((uint64_t)((uint32_t)(pos - d * a.WS) | (s << 29)) << 32);
+        const uint32_t q = (uint32_t)(pos - d * a.WS);
+        ne = a.far7 ? far7_pack(p, q, s, c7) : (uint64_t)p | ((uint64_t)(q | (s << 29)) << 32);
         if (a.inject && i == a.i_ml_end) {
           if (a.inject == 1) app = false;
-          else ne |= (uint64_t)0x1fffffffu << 32;  // q beyond the wave
+          else ne |= a.far7 ? (uint64_t)0xfffffffu << 30 : (uint64_t)0x1fffffffu << 32;  // q beyond the wave
         }
       }
     }
@@ -1630,13 +1724,13 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
 __global__ void __launch_bounds__(256) k_check_wave(const uint32_t* __restrict__ hitcnt, uint32_t ntiles_w,
                                                     uint32_t hcap, const uint64_t* __restrict__ far_in,
                                                     const uint32_t* __restrict__ far_in_count, uint32_t bcap,
-                                                    uint32_t WS, unsigned long long* rec_count, int* bad) {
+                                                    uint32_t WS, unsigned long long* rec_count, int* bad, int far7) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < ntiles_w) atomicAdd(rec_count, (unsigned long long)min(hitcnt[i], hcap));
   if (far_in) {
     const uint32_t nfar = min(*far_in_count, bcap);
     for (uint32_t j = i; j < nfar; j += gridDim.x * blockDim.x)
-      if (((uint32_t)(far_in[j] >> 32) & 0x1fffffffu) >= WS) atomicExch(bad, 1);
+      if (far_q(far_in[j], far7 != 0) >= WS) atomicExch(bad, 1);
   }
 }
 
@@ -1647,6 +1741,9 @@ __global__ void __launch_bounds__(256) k_check_wave(const uint32_t* __restrict__
 __device__ __forceinline__ uint64_t coprime30_upto(uint64_t n) {  // #{1 <= c <= n : gcd(c, 30) = 1}
   constexpr uint8_t cnt[30] = {0, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 4, 4, 4, 4, 5, 5, 6, 6, 6, 6, 7, 7, 7, 7, 7, 7, 8};
   return 8 * (n / 30) + cnt[n % 30];
+}
+__device__ __forceinline__ uint64_t coprime210_upto(uint64_t n) {  // #{1 <= c <= n : gcd(c, 210) = 1}
+  return coprime30_upto(n) - coprime30_upto(n / 7);  // c coprime to 30 and divisible by 7: c = 7c', c' coprime to 30
 }
 __device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {
   // fp64 estimate (off by at most one), exact fix on the remainder in
@@ -1659,7 +1756,8 @@ __device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {
 }
 __global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __restrict__ primes, uint64_t i0,
                                                           uint64_t i1, uint64_t x_lo, uint64_t x_hi,
-                                                          unsigned long long* __restrict__ out) {
+                                                          unsigned long long* __restrict__ out, uint64_t i7_lo,
+                                                          uint64_t i7_hi) {
   const uint64_t i = i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long cnt = 0;
   if (i < i1) {
@@ -1667,7 +1765,9 @@ __global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __rest
     uint64_t c_lo = div_floor(x_lo - 1, p) + 1;  // ceil(x_lo / p)
     if (c_lo < 2) c_lo = 2;
     const uint64_t c_hi = div_floor(x_hi, p);
-    if (c_hi >= c_lo) cnt = coprime30_upto(c_hi) - coprime30_upto(c_lo - 1);
+    if (c_hi >= c_lo)
+      cnt = i >= i7_lo && i < i7_hi ? coprime210_upto(c_hi) - coprime210_upto(c_lo - 1)  // primes skipping 7 | c
+                                    : coprime30_upto(c_hi) - coprime30_upto(c_lo - 1);
   }
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);

@@ -425,3 +425,31 @@ def test_random_large_geometries_invariants_and_mr(gpu_ctx):
     finally:
         gpu_ctx.set_max_base_pairs(1 << 27)
     assert ran >= 10
+
+
+@pytest.mark.parametrize("l,f,n", [(22, (1 << 37) - 4096, 300), (21, (1 << 26) - 2048, 300), (20, 1 << 21, 60)])
+def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
+    """Large primes may skip their multiples whose cofactor 7 divides (mod-210
+    far entries / ML states; those numbers are marked by the pattern of 7).
+    Every combination — both off (pure mod-30), default, both forced on —
+    gives the same table, and the large-prime invariants (records consumed ==
+    admissible multiples, counted coprime-210 where skipped) hold."""
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n)
+    results = []
+    for env in ({"ERATO_GPU_FAR7": "0", "ERATO_GPU_ML7": "0"}, {}, {"ERATO_GPU_ML7": "1"}):
+        old = {k: os.environ.get(k) for k in ("ERATO_GPU_FAR7", "ERATO_GPU_ML7")}
+        os.environ.update(env)
+        try:
+            st = gpu_ctx.count(p, check_invariants=True)
+            t, _ = gpu_ctx.table(p)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        results.append((st.prime_count, sha(t), st.large_records))
+    assert len({(c, h) for c, h, _ in results}) == 1
+    if l >= 21:  # fewer records are consumed when multiples of 7 are skipped
+        assert results[2][2] < results[0][2]
