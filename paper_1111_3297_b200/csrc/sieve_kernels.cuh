@@ -443,6 +443,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         cp_async_wait_all();
         const uint4 v0 = s_hits[warp * (kHitChunk / 4) + lane], v1 = s_hits[warp * (kHitChunk / 4) + 32 + lane];
         const uint32_t i0 = ch * kHitChunk + 4 * lane, i1 = i0 + 128;
+        EG_CHECK(i0 >= hcnt || (v0.x < S && (i0 + 3 >= hcnt || v0.w < S)), "hit record beyond the tile %u %u", v0.x, v0.w);
+        EG_CHECK(i1 >= hcnt || (v1.x < S && (i1 + 3 >= hcnt || v1.w < S)), "hit record beyond the tile %u %u", v1.x, v1.w);
         if (i1 + 3 < hcnt) {
           mark_a(tile_a, v0.x); mark_a(tile_a, v0.y); mark_a(tile_a, v0.z); mark_a(tile_a, v0.w);
           mark_a(tile_a, v1.x); mark_a(tile_a, v1.y); mark_a(tile_a, v1.z); mark_a(tile_a, v1.w);
@@ -1225,6 +1227,8 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
                    fe_a = smem_addr(sm.freg + base), fg_a = smem_addr(sm.fgofs);
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t t = lds_u8(fs_a + i);
+      EG_CHECK(t == kNoSlot || (t < a.ring && lds_u32(fg_a + 4 * t) + lds_u16(fr_a + 2 * i) < a.ring * a.bcap + NW * Sm::R),
+               "far bucket index out of range slot=%u", t);
       if (t != kNoSlot) a.far_buckets[lds_u32(fg_a + 4 * t) + lds_u16(fr_a + 2 * i)] = lds_u64(fe_a + 8 * i);
     }
   }
@@ -1237,6 +1241,8 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #pragma unroll kWriteUnroll
   for (uint32_t i = tid; i < total; i += NT) {
     const uint32_t key = lds_u32(srt_a + 4 * i);
+    EG_CHECK((key >> shift) < nb && lds_u32(gofs_a + 4 * (key >> shift)) + i < nb * a.hcap + NW * Sm::R,
+             "hit list index out of range key=%u", key);
     a.hits[lds_u32(gofs_a + 4 * (key >> shift)) + i] = key & smask;
   }
   // off/gofs/srt are rewritten only after the next round's first barrier
@@ -1356,6 +1362,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
             ++s;
             c7 = 2 * D2;
           }
+          EG_CHECK(c7 >= 1 && c7 <= 6 && pos < (1u << 30) + WS, "ML c7=%u pos=%u p=%u", c7, pos, p);
         }
       }
     }
@@ -1447,6 +1454,8 @@ __device__ __forceinline__ void scatter_far(const ScatterArgs& a, uint32_t blk, 
       const bool hi = r >= (int32_t)WS;
       r -= hi ? (int32_t)WS : 0;
       d += hi ? 1u : 0u;
+      EG_CHECK(!ok || (uint32_t)r < WS, "far next-hit remainder r=%d WS=%u p=%u q=%u", r, WS, p, q);
+      EG_CHECK(!FAR7 || !ok || (c7 >= 1 && c7 <= 6), "far c7=%u p=%u", c7, p);
       const bool keep = ok && d < left;
       uint32_t slot = a.wslot + d;
       if (slot >= ring) slot -= ring;

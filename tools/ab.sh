@@ -1,11 +1,11 @@
 #!/bin/bash
 # A/B timing of env-selected kernel variants (run on the GPU box):
-#   VARIANTS="ERATO_GPU_ML=rounds ERATO_GPU_ML=bins" CFGS="5 4" bash tools/ab.sh
+#   VARIANTS="DEFAULT=1 ERATO_GPU_FAR7=0,ERATO_GPU_ML7=0" CFGS="5 4" bash tools/ab.sh   (comma = several vars)
 # prints ms/step and the per-kernel split of a short bench run per variant.
 export PYTHONUNBUFFERED=1
 for c in ${CFGS:-5}; do
   for v in ${VARIANTS:-DEFAULT=1}; do
-    env $v timeout 300 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --no-table-e2e \
+    env $(echo "$v" | tr "," " ") timeout 300 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --no-table-e2e \
       --no-file-e2e --no-cfg4 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
