@@ -521,7 +521,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       if (valid) {
         uint32_t p, s;
         uint32_t q = med_first<P2>(cur, t, tf, x_t, combo_a, p, s);
-        if ((p << 3) > S) {
+#ifndef EG_TWO_HIT
+#define EG_TWO_HIT 1
+#endif
+        if (EG_TWO_HIT && (p << 1) > S) {  // p > S/2: hits are > S/2 apart, at most two in the tile
+          if (q < S) {
+            mark_a(tile_a, q);
+            q += wheel_D(s) * p;
+            if (q < S) mark_a(tile_a, q);
+          }
+        } else if ((p << 3) > S) {
           uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
           while (q < S) {
             mark_a(tile_a, q);
