@@ -58,11 +58,13 @@ ROOF = {
     4: (19_421_366_720, 7_608_331_782),
     5: (174_787_646_624, 37_185_502_020),
 }
-# This implementation's own work (tools/roofline_counts.py `ours_*`, mod-30
-# wheel, 2^20-bit tiles, 148-tile waves): hit records of large primes, of which
-# far primes (p > wave span) make FAR_RECORDS, and medium-prime marks.
-LARGE_RECORDS = {1: 0, 2: 0, 3: 20_188, 4: 835_065_655, 5: 7_429_219_143}
-FAR_RECORDS = {1: 0, 2: 0, 3: 0, 4: 0, 5: 1_789_110_090}
+# This implementation's own work (tools/roofline_counts.py `ours_*`, 2^20-bit
+# tiles, 148-tile waves): hit records of the ML primes (S < p <= wave span) and
+# of the far primes, each as (mod-30 wheel, mod 210: cofactors divisible by 7
+# skipped — stats.skip7 says which a run used), and medium-prime marks.
+# (cfg3's 37 primes just above the tile size are sieved as medium primes: no records)
+ML_RECORDS = {1: (0, 0), 2: (0, 0), 3: (0, 0), 4: (835_065_655, 715_771_037), 5: (5_640_109_053, 4_834_378_943)}
+FAR_RECORDS = {1: (0, 0), 2: (0, 0), 3: (0, 0), 4: (0, 0), 5: (1_789_110_090, 1_533_518_655)}
 MEDIUM_MARKS = {1: 2_704_493, 2: 2_151_023_657, 3: 673_975_296, 4: 5_391_802_774, 5: 21_567_210_790}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 # smem atomicOr/s per B200 at random word addresses (the sieve's bank-conflict
@@ -293,14 +295,15 @@ def roofline(m, world: int):
     }
     # ---- per-kernel: algorithmic bytes per launch / average launch time ----
     waves = max(ph.waves, 1)
-    recs = LARGE_RECORDS[cfg] / world
-    far = FAR_RECORDS[cfg] / world
+    far = FAR_RECORDS[cfg][1 if ph.skip7 & 1 else 0] / world
+    ml = ML_RECORDS[cfg][1 if ph.skip7 & 2 else 0] / world
+    recs = ml + far
     table_bytes = m["params"].table_bytes()
     alg = {
         # table written once + every hit record read once
         "k_tile": (table_bytes + 4.0 * recs) / waves,
         # ML records written + every ML state read and rewritten (8 B + 8 B) each wave
-        "k_scatter_ml": 4.0 * (recs - far) / waves + 16.0 * ph.ml_primes,
+        "k_scatter_ml": 4.0 * ml / waves + 16.0 * ph.ml_primes,
         # per far entry visited: 8 B entry in, 8 B re-bucketed entry out, 4 B record out
         "k_scatter_far": 20.0 * far / waves,
     }
@@ -314,7 +317,7 @@ def roofline(m, world: int):
         kernels[k] = {"alg_bytes_per_launch": round(alg[k]), "launch_us": round(launch_s[k] * 1e6, 2),
                       "achieved": round(ach, 1), "frac": round(ach / hbm, 4),
                       "traffic": (traffic or {}).get(k)}
-    tile_atoms = (MEDIUM_MARKS[cfg] + LARGE_RECORDS[cfg]) / world / waves
+    tile_atoms = MEDIUM_MARKS[cfg] / world / waves + recs / waves
     if launch_s["k_tile"] > 0:
         kernels["k_tile"]["smem_atomics_per_launch"] = round(tile_atoms)
         kernels["k_tile"]["atomic_rate"] = round(tile_atoms / launch_s["k_tile"], 1)

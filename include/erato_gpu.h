@@ -88,6 +88,8 @@ typedef struct {
   uint64_t medium_primes; /* base primes sieved inside the tiles (61 < p <= tile) */
   uint64_t ml_primes;     /* large primes walked every wave (tile < p <= wave span) */
   uint64_t far_primes;    /* large primes kept in the per-wave bucket ring (p > wave span) */
+  uint32_t skip7;         /* bit 0: far primes, bit 1: ML primes skip cofactors divisible by 7 (mod 210) */
+  uint32_t reserved0;
 } erato_gpu_stats;
 
 /* Count written to a caller's dev_count when a bucket / hit-list capacity
@@ -200,6 +202,12 @@ void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_ou
  * Writes up to cap primes to host dst; returns the count in *count. */
 int erato_gpu_extract_primes(erato_gpu_ctx* ctx, unsigned l, uint64_t f, uint64_t n,
                              unsigned flags, uint64_t* dst, uint64_t cap, uint64_t* count);
+
+/* The device base-prime list: the odd primes <= limit (limit <= 2^32 - 1),
+ * ascending, computed exactly as a run computes its base primes
+ * (build_base / simple_sieve(isqrt v), src/base.cpp:19-53, src/oracle.cpp:8-23):
+ * writes up to cap of them to host dst, *count = their number. */
+int erato_gpu_base_primes(erato_gpu_ctx* ctx, uint64_t limit, uint32_t* dst, uint64_t cap, uint64_t* count);
 
 /* ---- multi-GPU run_sieve -------------------------------- */
 /* num_gpus contiguous range shards (erato_gpu_shard), one host thread and one

@@ -23,7 +23,7 @@ EXPORTS = (
     "erato_gpu_count", "erato_gpu_write_table", "erato_gpu_shard", "erato_gpu_extract_primes",
     "erato_gpu_first_hit", "erato_gpu_set_max_base_pairs", "erato_gpu_run_to_sink",
     "erato_gpu_multi_create", "erato_gpu_multi_destroy", "erato_gpu_multi_uses_nccl",
-    "erato_gpu_multi_count", "erato_gpu_multi_write_table",
+    "erato_gpu_multi_count", "erato_gpu_multi_write_table", "erato_gpu_base_primes",
 )
 
 COUNT_OVERFLOW = (1 << 64) - 1  # ERATO_GPU_COUNT_OVERFLOW
@@ -42,7 +42,7 @@ class Stats(C.Structure):
         ("kernel_launches", C.c_uint32), ("retries", C.c_uint32),
         ("gen_s", C.c_double), ("bin_s", C.c_double), ("large_records", C.c_uint64),
         ("masks_s", C.c_double), ("medium_primes", C.c_uint64), ("ml_primes", C.c_uint64),
-        ("far_primes", C.c_uint64),
+        ("far_primes", C.c_uint64), ("skip7", C.c_uint32), ("reserved0", C.c_uint32),
     ]
 
 
@@ -116,5 +116,7 @@ def load(path: str = SO_PATH):
     L.erato_gpu_multi_write_table.restype = C.c_int
     L.erato_gpu_multi_write_table.argtypes = [C.c_void_p, C.c_char_p, C.c_uint, C.c_uint64, C.c_uint64, C.c_uint,
                                               C.c_char_p, C.c_size_t, u64p, C.POINTER(Stats)]
+    L.erato_gpu_base_primes.restype = C.c_int
+    L.erato_gpu_base_primes.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32), C.c_uint64, u64p]
     _lib = L
     return L

@@ -386,6 +386,55 @@ int compact_zeros(erato_gpu_ctx* c, cudaStream_t st, const uint32_t* bits, uint6
   return 0;
 }
 
+// build_base's simple_sieve(isqrt v) (src/base.cpp:19-53, src/oracle.cpp:8-23) on
+// the device: the odd numbers 1..vroot sieved by the tile kernel (multiples
+// from p^2), then a popcount-scan compaction into c->primes (ascending u32);
+// the count lands in scal[0].
+int base_primes(erato_gpu_ctx* c, cudaStream_t st, uint64_t vroot, uint32_t& launches) {
+  uint64_t* d_scal = c->scal.as<uint64_t>();
+  const uint64_t nbase_bits = (vroot + 1) / 2;  // odd numbers 1..vroot
+  const uint64_t prime_cap = pi_upper(vroot) + 64;
+  CUDA_TRY(c->primes.ensure(prime_cap * 4));
+  if (nbase_bits <= 1) {
+    CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
+    return 0;
+  }
+  const uint64_t words = ((nbase_bits + ((1u << kBaseLogTile) - 1)) >> kBaseLogTile) << (kBaseLogTile - 5);
+  CUDA_TRY(c->base_bits.ensure(words * 4));
+  const uint64_t rr = isqrt_u64(vroot);
+  // small primes in (61, rr]
+  const auto b61 = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), 61u) - c->h_sp.begin();
+  const auto brr = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), (uint32_t)std::min<uint64_t>(rr, 65535)) -
+                   c->h_sp.begin();
+  eg::TileArgs ta{};
+  ta.g0 = 0;
+  ta.tbits = nbase_bits;
+  ta.tile0 = 0;
+  ta.log_s = kBaseLogTile;
+  ta.med = c->spm.as<uint4>() + b61;
+  ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
+  {
+    auto idx_below = [&](uint32_t x) {  // medium-list index of the first prime >= x
+      const int64_t i = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), x) - c->h_sp.begin();
+      return (uint64_t)std::max<int64_t>(i - b61, 0);
+    };
+    ta.nmed_warp = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(idx_below((1u << kBaseLogTile) / 64), ta.nmed),
+                                                eg::kMaxWarpPrimes);
+    group_split(ta, idx_below((1u << kBaseLogTile) / 256), idx_below((1u << kBaseLogTile) / 128));
+  }
+  ta.ptab = c->ptab.as<uint32_t>();
+  ta.table = c->base_bits.as<uint32_t>();
+  ta.count = reinterpret_cast<unsigned long long*>(d_scal + 20);
+  const uint64_t bt = (nbase_bits + (1u << kBaseLogTile) - 1) >> kBaseLogTile;
+  launch_tiles(st, ta, (uint32_t)bt, true);
+  ++launches;
+  const int rc = compact_zeros<uint32_t>(c, st, c->base_bits.as<uint32_t>(), nbase_bits, 1, 1,
+                                         c->primes.as<uint32_t>(), prime_cap, d_scal + 0);
+  if (rc) return rc;
+  launches += 3;
+  return 0;
+}
+
 struct Plan {
   unsigned l;
   uint64_t f, n, u, v, T, g0;
@@ -558,52 +607,14 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     const uint64_t vroot = isqrt_u64(P.v);
     CUDA_TRY(cudaEventRecord(c->ev[0], st));
     // ---------------- 1-2. base primes <= sqrt(v) ----------------
-    uint64_t nbase_bits = (vroot + 1) / 2;  // odd numbers 1..vroot
-    const uint64_t prime_cap = pi_upper(vroot) + 64;
-    CUDA_TRY(c->primes.ensure(prime_cap * 4));
     // [0] total primes, [8..15] bounds + largest prime, [16] count, [17] overflow,
     // [18] hit records consumed, [19] expected records, [20] base-sieve count, [21] bad far entry,
     // [22] pattern-phase ns (PHASE_TIMING), [24..30] class thresholds, [40] compaction total
     uint64_t* d_scal = c->scal.as<uint64_t>();
     CUDA_TRY(cudaMemsetAsync(d_scal + 18, 0, 16, st));
     CUDA_TRY(cudaMemsetAsync(d_scal + 21, 0, 8, st));
-    if (nbase_bits > 1) {
-      const uint64_t words = ((nbase_bits + ((1u << kBaseLogTile) - 1)) >> kBaseLogTile) << (kBaseLogTile - 5);
-      CUDA_TRY(c->base_bits.ensure(words * 4));
-      const uint64_t rr = isqrt_u64(vroot);
-      // small primes in (61, rr]
-      const auto b61 = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), 61u) - c->h_sp.begin();
-      const auto brr = std::upper_bound(c->h_sp.begin(), c->h_sp.end(), (uint32_t)std::min<uint64_t>(rr, 65535)) -
-                       c->h_sp.begin();
-      eg::TileArgs ta{};
-      ta.g0 = 0;
-      ta.tbits = nbase_bits;
-      ta.tile0 = 0;
-      ta.log_s = kBaseLogTile;
-      ta.med = c->spm.as<uint4>() + b61;
-      ta.nmed = brr > b61 ? (uint32_t)(brr - b61) : 0;
-      {
-        auto idx_below = [&](uint32_t x) {  // medium-list index of the first prime >= x
-          const int64_t i = std::lower_bound(c->h_sp.begin(), c->h_sp.end(), x) - c->h_sp.begin();
-          return (uint64_t)std::max<int64_t>(i - b61, 0);
-        };
-        ta.nmed_warp = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(idx_below((1u << kBaseLogTile) / 64), ta.nmed),
-                                                    eg::kMaxWarpPrimes);
-        group_split(ta, idx_below((1u << kBaseLogTile) / 256), idx_below((1u << kBaseLogTile) / 128));
-      }
-      ta.ptab = c->ptab.as<uint32_t>();
-      ta.table = c->base_bits.as<uint32_t>();
-      ta.count = reinterpret_cast<unsigned long long*>(d_scal + 20);
-      const uint64_t bt = (nbase_bits + (1u << kBaseLogTile) - 1) >> kBaseLogTile;
-      launch_tiles(st, ta, (uint32_t)bt, true);
-      ++launches;
-      rc = compact_zeros<uint32_t>(c, st, c->base_bits.as<uint32_t>(), nbase_bits, 1, 1, c->primes.as<uint32_t>(),
-                                   prime_cap, d_scal + 0);
-      if (rc) return rc;
-      launches += 3;
-    } else {
-      CUDA_TRY(cudaMemsetAsync(d_scal, 0, 8, st));
-    }
+    rc = base_primes(c, st, vroot, launches);
+    if (rc) return rc;
     // ---------------- 3. class boundaries (one host sync) ----------------
     // index of the first prime above 61, S/64, S, MW*WS, max(WS/8, S), S/256, S/128
     uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, (uint64_t)P.MW * P.WS, std::max<uint64_t>(P.WS / 8, P.S),
@@ -1027,6 +1038,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       stats->medium_primes = nmed;
       stats->ml_primes = nml;
       stats->far_primes = nfar;
+      stats->skip7 = (far7 ? 1u : 0u) | (ml7 ? 2u : 0u);
       stats->base_primes = nprimes;
       stats->tiles = P.ntiles;
       stats->log_tile = P.log_s;
@@ -1462,5 +1474,23 @@ extern "C" int erato_gpu_multi_write_table(erato_gpu_multi* m, const char* out_d
     return rc;
   }
   if (path_out && path_cap) std::snprintf(path_out, path_cap, "%s", path.c_str());
+  return 0;
+}
+
+// The device base-prime list of a run (the odd primes <= limit, ascending):
+// build_base / simple_sieve(isqrt v) (src/base.cpp:19-53) as run_impl computes it.
+extern "C" int erato_gpu_base_primes(erato_gpu_ctx* c, uint64_t limit, uint32_t* dst, uint64_t cap, uint64_t* count) {
+  if (!c) return fail(ERATO_GPU_E_INVALID_ARG, "ctx is NULL");
+  if (limit > UINT32_MAX) return fail(ERATO_GPU_E_INVALID_ARG, "limit above 2^32");
+  CUDA_TRY(cudaSetDevice(c->device));
+  uint32_t launches = 0;
+  const int rc = base_primes(c, c->stream, limit, launches);
+  if (rc) return rc;
+  uint64_t n = 0;
+  CUDA_TRY(cudaMemcpyAsync(&n, c->scal.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const uint64_t m = std::min(n, cap);
+  if (dst && m) CUDA_TRY(cudaMemcpy(dst, c->primes.p, m * 4, cudaMemcpyDeviceToHost));
+  if (count) *count = n;
   return 0;
 }

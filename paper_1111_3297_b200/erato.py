@@ -214,6 +214,7 @@ class RunStats:
     medium_primes: int = 0
     ml_primes: int = 0
     far_primes: int = 0
+    skip7: int = 0
 
     @classmethod
     def _from(cls, s: _lib.Stats) -> "RunStats":
@@ -224,7 +225,8 @@ class RunStats:
                    large_s=s.large_s, output_s=s.output_s, total_s=s.total_s, base_primes=s.base_primes,
                    tiles=s.tiles, log_tile=s.log_tile, waves=s.waves, kernel_launches=s.kernel_launches,
                    retries=s.retries, gen_s=s.gen_s, bin_s=s.bin_s, large_records=s.large_records,
-                   medium_primes=s.medium_primes, ml_primes=s.ml_primes, far_primes=s.far_primes)
+                   medium_primes=s.medium_primes, ml_primes=s.ml_primes, far_primes=s.far_primes,
+                   skip7=s.skip7)
 
 
 @dataclass
@@ -342,6 +344,19 @@ class Context:
         _check(L.erato_gpu_extract_primes(self._h, params.l, params.f, params.n, params.flags,
                                           out.ctypes.data_as(_lib.u64p), cap, C.byref(cnt)))
         return out[:min(cap, cnt.value)]
+
+
+def base_primes(limit: int, device: int = 0) -> np.ndarray:
+    """The device base-prime list: odd primes <= limit, ascending (build_base's
+    simple_sieve, src/base.cpp:19-53), as a run computes them."""
+    ctx = context(device)
+    L = _lib.load()
+    cnt = C.c_uint64()
+    _check(L.erato_gpu_base_primes(ctx.handle, limit, None, 0, C.byref(cnt)))
+    out = np.empty(max(cnt.value, 1), dtype=np.uint32)
+    _check(L.erato_gpu_base_primes(ctx.handle, limit, out.ctypes.data_as(C.POINTER(C.c_uint32)), cnt.value,
+                                   C.byref(cnt)))
+    return out[:cnt.value]
 
 
 class MultiGPU:

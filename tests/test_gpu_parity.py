@@ -453,3 +453,15 @@ def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
     assert len({(c, h) for c, h, _ in results}) == 1
     if l >= 21:  # fewer records are consumed when multiples of 7 are skipped
         assert results[2][2] < results[0][2]
+
+
+@pytest.mark.parametrize("limit", [4096, 92681, 1049087, 16777471, 1073741839])
+def test_base_prime_list_equals_reference_simple_sieve(reference, limit):
+    """The device base-prime list (odd primes <= isqrt(v) of cfg1..cfg5),
+    element for element against the reference's simple_sieve
+    (src/oracle.cpp:8-23, the list build_base uses, src/base.cpp:23)."""
+    import paper_1111_3297_b200 as E
+    got = E.erato.base_primes(limit)
+    ref = reference.simple_sieve(limit)
+    ref = ref[ref > 2]
+    assert len(got) == len(ref) and np.array_equal(got, ref)

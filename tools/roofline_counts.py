@@ -41,6 +41,12 @@ def coprime30_upto(x: np.ndarray) -> np.ndarray:
     return 8 * (x // 30) + _T30[x % 30]
 
 
+def coprime210_upto(x: np.ndarray) -> np.ndarray:
+    """#{1 <= c <= x : gcd(c, 210) = 1}: coprime to 30, minus the multiples 7c' with c' coprime to 30."""
+    x = np.maximum(x, 0)
+    return coprime30_upto(x) - coprime30_upto(x // 7)
+
+
 def odd_upto(x: np.ndarray) -> np.ndarray:
     return (np.maximum(x, 0) + 1) // 2
 
@@ -76,6 +82,11 @@ def counts(l: int, f: int, n: int, log_tile: int = 20, wave_tiles: int = 148):
     if (u * u) <= v:
         lo2 = np.maximum(lo2, np.where(primes <= S, primes, 2))
     ours_marks = coprime30_upto(hi) - coprime30_upto(lo2 - 1)
+    # large primes skipping cofactors divisible by 7 (mod-210 far entries / ML states)
+    ours_marks210 = coprime210_upto(hi) - coprime210_upto(lo2 - 1)
+    WSb = wave_tiles * S
+    ml = (primes > S) & (primes <= WSb)
+    far = primes > WSb
     return {
         "l": l, "f": f, "n": n, "table_bits": T, "base_primes": int(len(primes)),
         "ref_wheel_marks": A_wheel, "ref_dense_marks": A_dense, "ref_large_hits": H_large,
@@ -84,6 +95,9 @@ def counts(l: int, f: int, n: int, log_tile: int = 20, wave_tiles: int = 148):
         "ours_large_records": int(ours_marks[ours_large].sum()),
         # far primes (p > WS = wave_tiles * 2^log_tile) reach the wave through the bucket ring
         "ours_far_records": int(ours_marks[primes > wave_tiles * S].sum()),
+        "ours_ml_records_mod30": int(ours_marks[ml].sum()),
+        "ours_ml_records_mod210": int(ours_marks210[ml].sum()),
+        "ours_far_records_mod210": int(ours_marks210[far].sum()),
         "ours_log_tile": log_tile,
         "ours_wave_tiles": wave_tiles,
     }
