@@ -73,7 +73,8 @@ METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roo
 # profiles/r02_microbench_atomics.log
 R_ATOM_MEASURED = 4.06e12
 NCU_TRAFFIC_FILE = os.path.join(HERE, "profiles", "ncu_traffic.json")
-KERNEL_SOURCES = [os.path.join(HERE, "paper_1111_3297_b200", "csrc", x) for x in ("sieve_kernels.cuh", "erato_gpu.cu")]
+# the device code of the wave kernels (a capture of other device code is not used)
+KERNEL_SOURCES = [os.path.join(HERE, "paper_1111_3297_b200", "csrc", "sieve_kernels.cuh")]
 
 
 def peaks():
@@ -189,9 +190,18 @@ class Rank:
         import paper_1111_3297_b200 as E
         self.torch, self.dist, self.E = torch, dist, E
         self.rank, self.world, self.local = dist_env()
+        # BENCH_TEST_SAME_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to
+        # exercise the multi-rank path on a 1-GPU box (NCCL refuses two ranks per GPU);
+        # such a line is marked "test_topology" and is not a scaling measurement
+        self.test_topology = os.environ.get("BENCH_TEST_SAME_DEVICE") == "1" and self.world > 1
+        if self.test_topology:
+            self.local = 0
         torch.cuda.set_device(self.local)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.test_topology:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
         self.dev = torch.device("cuda", self.local)
         self.ctx = E.Context(self.local)
         self.stream = torch.cuda.current_stream(self.dev)
@@ -204,7 +214,8 @@ class Rank:
     def allreduce(self, x: float, op: str = "max", dtype=None):
         if self.world == 1:
             return x
-        t = self.torch.tensor([x], dtype=dtype or self.torch.float64, device=self.dev)
+        t = self.torch.tensor([x], dtype=dtype or self.torch.float64,
+                              device="cpu" if self.test_topology else self.dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
         return t.item()
 
@@ -231,7 +242,12 @@ def measure(R: Rank, cfg: int, steps: int, warmup: int):
                                        C.c_void_p(R.stream.cuda_stream), 1, C.byref(st))
         E.erato._check(rc)
         if R.world > 1:
-            R.dist.all_reduce(count, op=R.dist.ReduceOp.SUM)
+            if R.test_topology:  # gloo: through the host
+                c = count.cpu()
+                R.dist.all_reduce(c, op=R.dist.ReduceOp.SUM)
+                count.copy_(c)
+            else:
+                R.dist.all_reduce(count, op=R.dist.ReduceOp.SUM)
         return st
 
     st = None
@@ -423,7 +439,8 @@ def run_ours(args):
         "config": {"workload": CONFIG_NAMES[args.config], "l": CONFIGS[args.config][0], "f": CONFIGS[args.config][1],
                    "n": CONFIGS[args.config][2], "numbers": head["numbers"]},
         "count": head["count"],
-        "parallelism": f"range-shard x{world} (one rank per GPU, NCCL all-reduce of the count)",
+        "parallelism": f"range-shard x{world} (one rank per GPU, NCCL all-reduce of the count)"
+                       + (" [TEST TOPOLOGY: all ranks on cuda:0 over gloo]" if R.test_topology else ""),
         "l2": "flushed between steps (256 MiB write, untimed); working set > L2",
         "e2e": {"value": head["numbers"] / t_e2e, "unit": "numbers/s", "h2d_bytes_per_step": 32 * world,
                 "d2h_bytes_per_step": 8 * world,

@@ -9,12 +9,12 @@ export PYTHONUNBUFFERED=1
 mkdir -p gpurun_out
 CFG=${CFG:-5}
 TAG=${TAG:-cur}
-timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-table-e2e \
+timeout 300 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-table-e2e --no-file-e2e --no-cfg4 \
   > gpurun_out/prof_plain_$TAG.json 2> gpurun_out/prof_plain_$TAG.err || exit 1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file gpurun_out/launches_cfg${CFG}_$TAG.csv \
-  python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-table-e2e > gpurun_out/ncu_launch_$TAG.log 2>&1
+  python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-table-e2e --no-file-e2e --no-cfg4 > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_tile|k_scatter" \
   --launch-skip ${SKIP:-300} --launch-count 3 -o gpurun_out/full_cfg${CFG}_$TAG -f \
-  python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-table-e2e > gpurun_out/ncu_full_$TAG.log 2>&1
+  python bench.py --config $CFG --steps 1 --warmup 0 --no-cpu-baseline --no-table-e2e --no-file-e2e --no-cfg4 > gpurun_out/ncu_full_$TAG.log 2>&1
 echo prof done
