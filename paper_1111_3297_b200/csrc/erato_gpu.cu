@@ -108,6 +108,8 @@ struct erato_gpu_ctx {
   // grow-only run buffers
   DevBuf base_bits, primes, med, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
   DevBuf recs, rcount, frecs, fslot, fcount;  // k_gen -> k_bin per-warp regions
+  DevBuf fst, wbuf, wcnt;                     // windowed far path: prime states, per-wave record buckets
+  DevBuf mlrec, mlcnt;                        // k_ml_emit: unsorted ML records of the wave, kMlSub buckets
   double hcap_scale = 1.0, bcap_scale = 1.0;
   uint64_t max_base_pairs = uint64_t{1} << 27;  // base.hpp:87
   cudaEvent_t ev[4] = {};
@@ -276,6 +278,8 @@ int create_impl(erato_gpu_ctx* c) {
     CUDA_TRY(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::MlSmem)));
   for (auto kf : {eg::k_scatter_far<false>, eg::k_scatter_far<true>})
     CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::FarSmem)));
+  for (auto kw : {eg::k_far_walk<false>, eg::k_far_walk<true>})
+    CUDA_TRY(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::WkSmem)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure((8192 + eg::kMedPad) * 16));
@@ -322,7 +326,8 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   if (c->xstream) cudaStreamSynchronize(c->xstream);
   for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
-                    &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount, &c->slices})
+                    &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount, &c->slices, &c->fst,
+                    &c->wbuf, &c->wcnt, &c->mlrec, &c->mlcnt})
     b->release();
   if (c->hslots) cudaFreeHost(c->hslots);
   if (c->hflags) cudaFreeHost(c->hflags);
@@ -601,6 +606,20 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
   P.WS = P.W * P.S;
   P.nwaves = (P.ntiles + P.W - 1) / P.W;
   P.MW = 1;  // (an ML walk over 2 waves per launch measured 2 ms slower at cfg5)
+  // Far primes: the windowed two-level path (k_far_walk + k_wave_sort) unless
+  // ERATO_GPU_FAR=ring asks for the per-wave bucket ring (k_scatter_far) or
+  // the k_gen/k_bin fallback is forced.  In window mode the far class starts
+  // at WS / far_div: ML primes that hit a wave less than ~far_div/2 times
+  // cost more per record in the per-wave walk than through the two levels.
+  const char* sc_env0 = std::getenv("ERATO_GPU_SCATTER");
+  const char* fm_env = std::getenv("ERATO_GPU_FAR");
+  const bool win = !(fm_env && std::strcmp(fm_env, "ring") == 0) && !(sc_env0 && std::strcmp(sc_env0, "genbin") == 0) &&
+                   P.W <= (uint32_t)eg::kScBins;
+  uint32_t far_div = 1;
+  if (const char* e = std::getenv("ERATO_GPU_FAR_DIV")) far_div = (uint32_t)std::max(1, std::atoi(e));
+  uint32_t kwin_max = 64;
+  if (const char* e = std::getenv("ERATO_GPU_FAR_WINDOW")) kwin_max = (uint32_t)std::max(1, std::atoi(e));
+  kwin_max = std::min<uint32_t>(kwin_max, eg::kScBins);
 
   uint32_t launches = 0;
   for (int attempt = 0;; ++attempt) {
@@ -617,7 +636,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     if (rc) return rc;
     // ---------------- 3. class boundaries (one host sync) ----------------
     // index of the first prime above 61, S/64, S, MW*WS, max(WS/8, S), S/256, S/128
-    uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, (uint64_t)P.MW * P.WS, std::max<uint64_t>(P.WS / 8, P.S),
+    const uint64_t p_ml = win ? std::max<uint64_t>(P.WS / far_div, P.S) : (uint64_t)P.MW * P.WS;  // largest ML prime
+    uint64_t thr[7] = {61, (uint64_t)P.S / 64, P.S, p_ml, std::max<uint64_t>(P.WS / 8, P.S),
                        (uint64_t)P.S / 256, (uint64_t)P.S / 128};
     CUDA_TRY(cudaMemcpyAsync(d_scal + 24, thr, sizeof(thr), cudaMemcpyHostToDevice, st));
     eg::k_bounds<<<1, 32, 0, st>>>(c->primes.as<uint32_t>(), d_scal + 0, d_scal + 24, 7, d_scal + 8);
@@ -647,6 +667,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     ++launches;
     const bool have_large = nml + nfar > 0;
     uint32_t ring = 1, bcap = 1, hcap = 4, rcap = 1, fcap = 1;
+    uint32_t kwin = 1, wcap = 4, wmagic = 0;  // window mode: waves per window, records per wave bucket
+    uint32_t mlcap = 4;                       // k_ml_emit: records per ML record bucket
     bool split = false, far7 = false, ml7 = false;
     if (have_large) {
       const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
@@ -655,11 +677,37 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
       CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
+      {
+        // k_ml_emit record buckets: expected ML records per wave / kMlSub (+15 % and slack)
+        const double sr_ml = std::max(0.0, std::log(std::log((double)std::max<uint64_t>(std::min<uint64_t>(p_ml, pmax), P.S + 1)) /
+                                                    std::log((double)P.S))) + 0.02;
+        const double em = (double)P.WS * (8.0 / 15.0) * sr_ml / eg::kMlSub;
+        mlcap = (uint32_t)std::min<double>((em * 1.15 + 8192) * c->hcap_scale, 1u << 28);
+        mlcap = (mlcap + 3) & ~3u;
+        CUDA_TRY(c->mlrec.ensure(((uint64_t)eg::kMlSub * mlcap + eg::kScTrash) * 4));
+        CUDA_TRY(c->mlcnt.ensure(eg::kMlSub * 4));
+        CUDA_TRY(cudaMemsetAsync(c->mlcnt.p, 0, eg::kMlSub * 4, st));
+      }
       // the lists of the MW waves of an ML window, + trash of the split scatter
       CUDA_TRY(c->hits.ensure(((uint64_t)P.MW * P.W * hcap + eg::kScTrash) * 4));
       CUDA_TRY(c->hitcnt.ensure((uint64_t)P.MW * P.W * 4));
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.MW * P.W * 4, st));
-      if (nfar) {
+      if (nfar && win) {
+        const char* f7 = std::getenv("ERATO_GPU_FAR7");
+        const bool w7 = !(f7 && std::strcmp(f7, "0") == 0);
+        const double sr_far = std::max(0.0, std::log(lnP / std::log((double)p_ml))) + 0.01;
+        const double ew = (double)P.WS * (8.0 / 15.0) * (w7 ? 6.0 / 7.0 : 1.0) * sr_far;  // records per wave
+        wcap = (uint32_t)std::min<double>((ew * 1.10 + 8192) * c->bcap_scale, 1u << 30);
+        wcap = (wcap + 3) & ~3u;
+        const uint64_t nwin = (P.nwaves + kwin_max - 1) / kwin_max;
+        kwin = (uint32_t)((P.nwaves + nwin - 1) / nwin);
+        while (kwin > 1 && ((uint64_t)kwin * wcap + eg::kScTrash >= (1ull << 32) || (uint64_t)kwin * wcap * 4 > (6ull << 30)))
+          kwin = (kwin + 1) / 2;
+        wmagic = (uint32_t)((1ull << 32) / P.W) + 1;  // umulhi(t, wmagic) = t / W for t * W < 2^32
+        CUDA_TRY(c->fst.ensure(nfar * 8));
+        CUDA_TRY(c->wbuf.ensure(((uint64_t)kwin * wcap + eg::kScTrash) * 4));
+        CUDA_TRY(c->wcnt.ensure((uint64_t)eg::kScBins * 4));
+      } else if (nfar) {
         // an entry's next hit lies at most 3p (mod 30) or 5p (mod 210: two wheel steps) ahead
         ring = (uint32_t)std::min<uint64_t>(6ull * pmax / P.WS + 3, P.nwaves + 2);
         if (ring > (uint32_t)eg::kMaxRing) return fail(ERATO_GPU_RANGE_TOO_LARGE, "far bucket ring exceeds 256 waves");
@@ -690,7 +738,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
       // far primes skip cofactors divisible by 7 (mod-210 entries) when p < 2^31 and q < 2^28 fit
       const char* f7_env = std::getenv("ERATO_GPU_FAR7");
-      far7 = split && nfar && pmax < (1u << 31) && P.WS <= (1u << 28) && !(f7_env && std::strcmp(f7_env, "0") == 0);
+      far7 = split && nfar && (win || (pmax < (1u << 31) && P.WS <= (1u << 28))) &&
+             !(f7_env && std::strcmp(f7_env, "0") == 0);
       // ML primes too (p < 2^28 and next-hit offsets < 6p < 2^30 need WS <= 170 * 2^20), when they all
       // hit a wave >= ~4 times (p <= WS/8: cfg4 -7% ML time); with primes up to WS (cfg5) the extra
       // data-dependent step in the walk costs more than the skipped records save (+13% measured)
@@ -718,6 +767,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       if (const char* inj = std::getenv("ERATO_GPU_TEST_INJECT")) sa.inject = std::atoi(inj);  // tests only
       sa.far7 = far7 ? 1 : 0;
       sa.ml7 = ml7 ? 1 : 0;
+      sa.fst = (win && nfar) ? c->fst.as<uint64_t>() : nullptr;
       const uint64_t nl = nprimes - iS;
       eg::k_setup_large<<<(unsigned)((nl + eg::kSetupThreads - 1) / eg::kSetupThreads), eg::kSetupThreads, 0, st>>>(sa);
       ++launches;
@@ -820,8 +870,55 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       ba.bcap = bcap;
       ba.overflow = ga.overflow;
     }
+    int sa_inject = 0;
+    if (const char* inj = std::getenv("ERATO_GPU_TEST_INJECT")) sa_inject = std::atoi(inj);  // tests only
     eg::ScatterArgs sca{};
-    uint32_t ml_blocks = c->nsm, far_blocks = c->nsm;
+    uint32_t ml_blocks = c->nsm, far_blocks = c->nsm, walk_blocks = c->nsm;
+    const bool winfar = win && nfar > 0;
+    const char* ml_env = std::getenv("ERATO_GPU_ML");
+    const bool emit = split && nml > 0 && ml_env && std::strcmp(ml_env, "emit") == 0;  // (measured slower: off by default)
+    uint32_t emit_blocks = c->nsm;
+    eg::MlEmitArgs mea{};
+    eg::FarWalkArgs fwa{};
+    eg::WaveSortArgs wsa{};
+    wsa.log_s = P.log_s;
+    wsa.hcap = hcap;
+    wsa.overflow = reinterpret_cast<int*>(d_scal + 17);
+    if (emit) {
+      int occ = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_ml_emit<false>, eg::kEmWarps * 32, 0));
+      const uint64_t units = (nml + 31) / 32;
+      emit_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+                                                 std::max<uint64_t>(1, (units + eg::kEmWarps - 1) / eg::kEmWarps));
+      mea.ml = c->ml.as<uint2>();
+      mea.nml = (uint32_t)nml;
+      mea.WS = P.WS;
+      mea.log_s = P.log_s;
+      mea.rec = c->mlrec.as<uint32_t>();
+      mea.cnt = c->mlcnt.as<uint32_t>();
+      mea.cap = mlcap;
+      mea.overflow = wsa.overflow;
+    }
+    if (winfar) {
+      int occ = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_far_walk<true>, eg::kWkWarps * 32,
+                                                             sizeof(eg::WkSmem)));
+      const uint64_t units = (nfar + 31) / 32;
+      walk_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+                                                 std::max<uint64_t>(1, (units + eg::kWkWarps - 1) / eg::kWkWarps));
+      fwa.primes = c->primes.as<uint32_t>() + iWS;
+      fwa.st = c->fst.as<uint64_t>();
+      fwa.nfar = (uint32_t)nfar;
+      fwa.span = (uint64_t)kwin * P.WS;
+      fwa.WS = P.WS;
+      fwa.log_s = P.log_s;
+      fwa.magic = wmagic;
+      fwa.wbuf = c->wbuf.as<uint32_t>();
+      fwa.wcnt = c->wcnt.as<uint32_t>();
+      fwa.wcap = wcap;
+      fwa.trash_at = kwin * wcap;
+      fwa.overflow = reinterpret_cast<int*>(d_scal + 17);
+    }
     if (split) {
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_scatter_ml<false>, eg::kMlWarps * 32,
@@ -868,7 +965,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         ga.ntiles_w = ntw;
         ba.ntiles_w = ntw;
         const uint32_t slot = nfar ? (uint32_t)(w % ring) : 0;
-        ga.far_in = nfar ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
+        ga.far_in = (nfar && !winfar) ? c->buckets.as<uint64_t>() + (uint64_t)slot * bcap : nullptr;
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
         // this wave's hit lists inside the ML window's lists
@@ -878,7 +975,12 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         ta.hits = hits_w;
         ta.hitcnt = hitcnt_w;
         if (split) {
-          if (nml && wi == 0) {  // ML walk over the window's tiles, state re-based by the window span
+          if (emit) {
+            mea.ntiles_w = ntw;
+            if (ml7) eg::k_ml_emit<true><<<emit_blocks, eg::kEmWarps * 32, 0, st>>>(mea);
+            else eg::k_ml_emit<false><<<emit_blocks, eg::kEmWarps * 32, 0, st>>>(mea);
+            launches += 1;
+          } else if (nml && wi == 0) {  // ML walk over the window's tiles, state re-based by the window span
             eg::ScatterArgs m = sca;
             m.ntiles_w = (uint32_t)std::min<uint64_t>((uint64_t)P.MW * P.W, P.ntiles - tile0);
             m.WS = P.MW * P.WS;
@@ -889,7 +991,41 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             launches += 1;
           }
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
-          if (nfar) {
+          uint32_t nseg = 0, max_cap = 0;  // record segments k_wave_sort partitions by tile
+          if (emit) {
+            for (int k = 0; k < eg::kMlSub; ++k) {
+              wsa.in[nseg] = c->mlrec.as<uint32_t>() + (uint64_t)k * mlcap;
+              wsa.in_count[nseg] = c->mlcnt.as<uint32_t>() + k;
+              wsa.cap[nseg] = mlcap;
+              ++nseg;
+            }
+            max_cap = mlcap;
+          }
+          if (winfar) {
+            const uint32_t wl = (uint32_t)(w % kwin);
+            if (wl == 0) {  // a new window: walk the far primes through its waves
+              const uint64_t tiles_left = P.ntiles - tile0;
+              fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
+              fwa.lim = std::min<uint64_t>((uint64_t)kwin * P.W, tiles_left) << P.log_s;
+              CUDA_TRY(cudaMemsetAsync(c->wcnt.p, 0, (uint64_t)eg::kScBins * 4, st));
+              if (far7) eg::k_far_walk<true><<<walk_blocks, eg::kWkWarps * 32, sizeof(eg::WkSmem), st>>>(fwa);
+              else eg::k_far_walk<false><<<walk_blocks, eg::kWkWarps * 32, sizeof(eg::WkSmem), st>>>(fwa);
+              launches += 1;
+              if (w == 0 && sa_inject == 2) eg::k_inject_wrec<<<1, 1, 0, st>>>(fwa.wbuf, fwa.wcnt);  // tests only
+            }
+            const uint32_t* in = c->wbuf.as<uint32_t>() + (uint64_t)wl * wcap;
+            const uint32_t* in_count = c->wcnt.as<uint32_t>() + wl;
+            if (flags & ERATO_GPU_CHECK_INVARIANTS) {
+              eg::k_check_wrecs<<<(unsigned)c->nsm, 256, 0, st>>>(in, in_count, wcap, ntw << P.log_s,
+                                                                  reinterpret_cast<int*>(d_scal + 21));
+              ++launches;
+            }
+            wsa.in[nseg] = in;
+            wsa.in_count[nseg] = in_count;
+            wsa.cap[nseg] = wcap;
+            ++nseg;
+            max_cap = std::max(max_cap, wcap);
+          } else if (nfar) {
             sca.wave = w;
             sca.wslot = slot;
             sca.ntiles_w = ntw;
@@ -899,6 +1035,14 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             sca.hitcnt = hitcnt_w;
             if (far7) eg::k_scatter_far<true><<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
             else eg::k_scatter_far<false><<<far_blocks, eg::kFarWarps * 32, sizeof(eg::FarSmem), st>>>(sca);
+            launches += 1;
+          }
+          if (nseg) {  // one chunk per CTA; CTAs past a segment's count exit
+            wsa.nb = ntw;
+            wsa.hits = hits_w;
+            wsa.hitcnt = hitcnt_w;
+            const uint32_t chunks = (max_cap + eg::kWsChunk - 1) / eg::kWsChunk;
+            eg::k_wave_sort<<<dim3(chunks, nseg), eg::kWsThreads, 0, st>>>(wsa);
             launches += 1;
           }
         } else {
@@ -915,10 +1059,11 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           ev_pairs.push_back({evi, true});
           evi += 3;
         }
-        ta.reset_bucket_count = nfar ? c->bcount.as<uint32_t>() + slot : nullptr;
+        ta.reset_bucket_count = (nfar && !winfar) ? c->bcount.as<uint32_t>() + slot : nullptr;
+        ta.reset_ml_count = emit ? c->mlcnt.as<uint32_t>() : nullptr;
         if (flags & ERATO_GPU_CHECK_INVARIANTS) {
           eg::k_check_wave<<<(unsigned)c->nsm, 256, 0, st>>>(
-              hitcnt_w, ntw, hcap, nfar ? ga.far_in : nullptr, ga.far_in_count, bcap, P.WS,
+              hitcnt_w, ntw, hcap, (nfar && !winfar) ? ga.far_in : nullptr, ga.far_in_count, bcap, P.WS,
               reinterpret_cast<unsigned long long*>(d_scal + 18), reinterpret_cast<int*>(d_scal + 21), far7 ? 1 : 0);
           ++launches;
         }

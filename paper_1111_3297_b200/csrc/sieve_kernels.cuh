@@ -238,6 +238,7 @@ struct TileArgs {
   uint64_t out_tile0;            //   table + (t - out_tile0) * S/32 (a wave slice when streaming)
   unsigned long long* count;     // zero-bit accumulator
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
+  uint32_t* reset_ml_count;      // the kMlSub record-bucket counters of k_ml_emit, consumed this wave (nullable)
   unsigned long long* phase_ns;  // nullable: CTA 0 adds its pattern-phase time (masks_s)
 };
 
@@ -573,6 +574,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     if (HITS) a.hitcnt[blockIdx.x] = 0;
     if (blockIdx.x == 0 && a.reset_bucket_count) *a.reset_bucket_count = 0;
   }
+  if (blockIdx.x == 0 && tid < 8 && a.reset_ml_count) a.reset_ml_count[tid] = 0;  // (kMlSub = 8)
 
   // 4. popcount + write-out (count_zeros simd.cpp:18-25, segment_to_bytes
   // driver.cpp:22-27: LSB-first bytes == little-endian words)
@@ -1180,13 +1182,17 @@ __device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" : : "r"(addr), "r"(v) : "memory");
+}
 // if (key != kNoRec) *addr = key
 __device__ __forceinline__ void sts_if_rec(uint32_t addr, uint32_t key) {
   asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, -1; @q st.shared.u32 [%0], %1; }" : : "r"(addr), "r"(key)
                : "memory");
 }
 
-template <int NW, int SL, bool FAR>
+// COMPACT: the warp's staging holds n real records (no sentinels).
+template <int NW, int SL, bool FAR, bool COMPACT = false>
 __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterArgs& a, uint32_t n) {
   using Sm = ScSmem<NW, SL, FAR>;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1226,8 +1232,13 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #pragma unroll kPlaceUnroll
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t key = lds_u32(rg_a + 4 * i);
-      const uint32_t o = lds_u32(off_a + 4 * min(key >> shift, (uint32_t)kScBins - 1));  // sentinels: any bin
-      sts_if_rec(srt_a + 4 * (o + lds_u16(rk_a + 2 * i)), key);
+      if constexpr (COMPACT) {
+        const uint32_t o = lds_u32(off_a + 4 * (key >> shift));
+        sts_u32(srt_a + 4 * (o + lds_u16(rk_a + 2 * i)), key);
+      } else {
+        const uint32_t o = lds_u32(off_a + 4 * min(key >> shift, (uint32_t)kScBins - 1));  // sentinels: any bin
+        sts_if_rec(srt_a + 4 * (o + lds_u16(rk_a + 2 * i)), key);
+      }
     }
   }
   if constexpr (FAR) {
@@ -1272,6 +1283,9 @@ __device__ __forceinline__ void sc_flush(ScSmem<NW, SL, FAR>& sm, const ScatterA
 #ifndef EG_ML_PF
 #define EG_ML_PF 1
 #endif
+#ifndef EG_ML_COMPACT
+#define EG_ML_COMPACT 1
+#endif
 constexpr int kMlWarps = EG_ML_WARPS, kMlSteps = EG_ML_STEPS, kMlPf = EG_ML_PF;
 #ifndef EG_FAR_PF
 #define EG_FAR_PF 2
@@ -1280,8 +1294,9 @@ constexpr int kFarWarps = EG_FAR_WARPS, kFarSteps = EG_FAR_STEPS, kFarPf = EG_FA
 using MlSmem = ScSmem<kMlWarps, kMlSteps, false>;
 using FarSmem = ScSmem<kFarWarps, kFarSteps, true>;
 // records / entries one round may send to the trash area
-constexpr uint32_t kScTrash = (uint32_t)(MlSmem::R * kMlWarps > FarSmem::R * kFarWarps ? MlSmem::R * kMlWarps
-                                                                                       : FarSmem::R * kFarWarps);
+constexpr uint32_t kScTrash0 = (uint32_t)(MlSmem::R * kMlWarps > FarSmem::R * kFarWarps ? MlSmem::R * kMlWarps
+                                                                                        : FarSmem::R * kFarWarps);
+constexpr uint32_t kScTrash = kScTrash0 > 8192 ? kScTrash0 : 8192;  // (>= a k_far_walk round and a k_wave_sort chunk)
 
 __device__ __forceinline__ uint32_t rotr4(uint32_t x) { return __funnelshift_r(x, x, 4); }
 
@@ -1299,7 +1314,18 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   const uint32_t reg_a = smem_addr(sm.reg + warp * MlSmem::R + lane);
   const uint32_t rank_a = smem_addr(sm.rank + warp * MlSmem::R + lane);
   const uint32_t cnt_a = smem_addr(sm.cnt), sink_a = cnt_a + 4 * (kScBins + lane);
-  uint32_t u = blk * kMlWarps + warp;
+#ifndef EG_BOUS
+#define EG_BOUS 1
+#endif
+  // unit order of a warp: row k of nw units, alternately from the left and
+  // from the right (primes ascend, so hits per unit descend: pairing a dense
+  // unit of one row with a sparse one of the next evens out the warps' work)
+  const uint32_t gw0 = blk * kMlWarps + warp;
+  uint32_t urow = 0;
+  auto unit_at = [&](uint32_t k) -> uint32_t {
+    return k * nw + ((EG_BOUS && EG_ML_COMPACT && (k & 1)) ? nw - 1 - gw0 : gw0);
+  };
+  uint32_t u = gw0;
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nml;
   uint2 e0 = ok ? a.ml[idx] : make_uint2(0, 0);
@@ -1326,8 +1352,75 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
   };
   uint2 pf[kMlPf];
 #pragma unroll
-  for (int k = 0; k < kMlPf; ++k) pf[k] = load(u + (k + 1) * nw);
+  for (int k = 0; k < kMlPf; ++k) pf[k] = load(unit_at(k + 1));
   bool live = u < nu;  // warp-uniform
+#if EG_ML_COMPACT
+  // Compacted emission: a step's records go to consecutive staging slots
+  // (ballot + popc), so a round holds R real records per warp whatever the
+  // share of idle lanes, and the placement / write passes and the per-round
+  // scan, reservations and barriers are paid per record, not per lane slot.
+  uint32_t ltm;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+  const uint32_t regw_a = smem_addr(sm.reg + warp * MlSmem::R), rankw_a = smem_addr(sm.rank + warp * MlSmem::R);
+  for (;;) {
+    uint32_t kb = 0;  // staged records of this warp (warp-uniform)
+    while (live && kb <= (uint32_t)MlSmem::R - 32) {
+      const bool v = pos < B;
+      const uint32_t m = __ballot_sync(kFull, v);
+      if (!m) {
+        if (ok) a.ml[idx] = ML7 ? ml7_pack(p, pos - WS, s, c7) : make_uint2(p | ((s & 7) << 29), pos - WS);
+        ++urow;
+        u = unit_at(urow);
+        if (u >= nu) {
+          live = false;
+          break;
+        }
+        idx = u * 32 + lane;
+        ok = idx < a.nml;
+        decode(pf[0]);
+        dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+#pragma unroll
+        for (int k = 0; k + 1 < kMlPf; ++k) pf[k] = pf[k + 1];
+        pf[kMlPf - 1] = load(unit_at(urow + kMlPf));
+        continue;
+      }
+      const uint32_t slot = kb + __popc(m & ltm);
+      kb += __popc(m);
+      if (v) {
+        uint32_t r;
+        asm volatile(
+            "atom.shared.add.u32 %0, [%1], 1;\n\t"
+            "st.shared.u32 [%2], %3;"
+            : "=r"(r)
+            : "r"(cnt_a + ((pos >> shift) << 2)), "r"(regw_a + (slot << 2)), "r"(pos)
+            : "memory");
+        const uint32_t D = dd & 15u;
+        pos += D * p;
+        dd = rotr4(dd);
+        ++s;
+        if (ML7) {  // the next admissible cofactor may be divisible by 7: then take the one after
+          c7 += 2 * D;
+          c7 -= c7 >= 7 ? 7 : 0;
+          if (c7 == 0) {
+            const uint32_t D2 = dd & 15u;
+            pos += D2 * p;
+            dd = rotr4(dd);
+            ++s;
+            c7 = 2 * D2;
+          }
+          EG_CHECK(c7 >= 1 && c7 <= 6 && pos < (1u << 30) + WS, "ML c7=%u pos=%u p=%u", c7, pos, p);
+        }
+        st_rank(rankw_a + (slot << 1), r);
+      }
+    }
+    const int more = __syncthreads_or(live);
+    sc_flush<kMlWarps, kMlSteps, false, true>(sm, a, kb);
+    if (!more) break;
+  }
+  (void)reg_a;
+  (void)rank_a;
+  (void)sink_a;
+#else
   for (;;) {
     bool rk_pend = false;  // the last staged rank is stored one step late
     uint32_t rk_addr = 0, rk_val = 0;
@@ -1381,6 +1474,7 @@ __device__ __forceinline__ void scatter_ml(const ScatterArgs& a, uint32_t blk, u
     sc_flush(sm, a, k);
     if (!more) break;
   }
+#endif
 }
 
 template <bool FAR7>
@@ -1502,6 +1596,445 @@ template <bool FAR7>
 __global__ void __launch_bounds__(kFarWarps * 32, EG_FAR_MINB) k_scatter_far(const ScatterArgs a) {
   extern __shared__ uint4 smem_raw[];
   scatter_far<FAR7>(a, blockIdx.x, gridDim.x, *reinterpret_cast<FarSmem*>(smem_raw));
+}
+
+// ---------------------------------------------------------------------------
+// ML primes, generator only (default): k_ml_emit walks the ML primes exactly
+// like k_scatter_ml but appends the wave's hit records UNSORTED to one of
+// kMlSub record buckets — a warp stages up to R compacted records in shared
+// memory, reserves a run with one global atomicAdd and copies it out in
+// 128-byte rows, without any CTA-wide barrier — and k_wave_sort partitions
+// them by tile together with the wave's far records.  The sort is a dense
+// kernel (every lane holds a record), so splitting generation from
+// partitioning costs fewer instructions per record than sorting each
+// scatter round in the walking CTA.
+constexpr int kMlSub = 8;
+struct MlEmitArgs {
+  uint2* ml;  // ML primes, ascending: {p | s << 29, pos}
+  uint32_t nml;
+  uint32_t WS, ntiles_w, log_s;
+  uint32_t* rec;  // [kMlSub][cap] + trash
+  uint32_t* cnt;  // [kMlSub]
+  uint32_t cap;
+  int* overflow;
+};
+#ifndef EG_EM_WARPS
+#define EG_EM_WARPS 8
+#endif
+#ifndef EG_EM_STEPS
+#define EG_EM_STEPS 12
+#endif
+constexpr int kEmWarps = EG_EM_WARPS, kEmR = EG_EM_STEPS * 32;
+
+template <bool ML7>
+__global__ void __launch_bounds__(kEmWarps * 32) k_ml_emit(const MlEmitArgs a) {
+  __shared__ uint32_t s_stage[kEmWarps][kEmR];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t WS = a.WS;
+  const uint32_t B = a.ntiles_w << a.log_s;  // walk bound (the end of the last tile in the last wave)
+  const uint32_t nw = gridDim.x * kEmWarps;
+  const uint32_t nu = (a.nml + 31) / 32;
+  const uint32_t gw0 = blockIdx.x * kEmWarps + warp;
+  const uint32_t sub = gw0 % kMlSub;
+  const uint32_t st_a = smem_addr(&s_stage[warp][0]);
+  uint32_t ltm;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+  uint32_t urow = 0;
+  auto unit_at = [&](uint32_t k) -> uint32_t { return k * nw + ((EG_BOUS && (k & 1)) ? nw - 1 - gw0 : gw0); };
+  uint32_t u = gw0;
+  if (u >= nu) return;
+  uint32_t idx = u * 32 + lane;
+  bool ok = idx < a.nml;
+  auto load = [&](uint32_t uu) -> uint2 {
+    const uint32_t j = uu * 32 + lane;
+    return (uu < nu && j < a.nml) ? a.ml[j] : make_uint2(0, 0);
+  };
+  uint32_t p, pos, s, c7 = 0;
+  auto decode = [&](uint2 e) {
+    if (ML7) {
+      p = e.x & 0x0fffffffu;
+      s = (e.x >> 28) & 7;
+      c7 = (e.x >> 31) | ((e.y >> 30) << 1);
+      pos = ok ? e.y & 0x3fffffffu : B;
+    } else {
+      p = e.x & 0x1fffffffu;
+      s = e.x >> 29;
+      pos = ok ? e.y : B;
+    }
+  };
+  decode(load(u));
+  uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
+  uint2 pf = load(unit_at(1));
+  uint32_t kb = 0;  // staged records of this warp (warp-uniform)
+  auto flush = [&]() {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&a.cnt[sub], kb);
+    base = __shfl_sync(kFull, base, 0);
+    const bool over = base + kb > a.cap;
+    if (over && lane == 0) atomicExch(a.overflow, 1);
+    uint32_t* dst = a.rec + (over ? (size_t)kMlSub * a.cap : (size_t)sub * a.cap + base);
+    __syncwarp();
+    for (uint32_t i = lane; i < kb; i += 32) dst[i] = lds_u32(st_a + 4 * i);
+    __syncwarp();
+    kb = 0;
+  };
+  for (;;) {
+    const bool v = pos < B;
+    const uint32_t m = __ballot_sync(kFull, v);
+    if (!m) {
+      if (ok) a.ml[idx] = ML7 ? ml7_pack(p, pos - WS, s, c7) : make_uint2(p | ((s & 7) << 29), pos - WS);
+      ++urow;
+      u = unit_at(urow);
+      if (u >= nu) break;
+      idx = u * 32 + lane;
+      ok = idx < a.nml;
+      decode(pf);
+      dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+      pf = load(unit_at(urow + 1));
+      continue;
+    }
+    if (v) {
+      sts_u32(st_a + 4 * (kb + __popc(m & ltm)), pos);
+      const uint32_t D = dd & 15u;
+      pos += D * p;
+      dd = rotr4(dd);
+      ++s;
+      if (ML7) {  // the next admissible cofactor may be divisible by 7: then take the one after
+        c7 += 2 * D;
+        c7 -= c7 >= 7 ? 7 : 0;
+        if (c7 == 0) {
+          const uint32_t D2 = dd & 15u;
+          pos += D2 * p;
+          dd = rotr4(dd);
+          ++s;
+          c7 = 2 * D2;
+        }
+        EG_CHECK(c7 >= 1 && c7 <= 6 && pos < (1u << 30) + WS, "ML c7=%u pos=%u p=%u", c7, pos, p);
+      }
+    }
+    kb += __popc(m);
+    if (kb > (uint32_t)kEmR - 32) flush();
+  }
+  if (kb) flush();
+}
+
+// ---------------------------------------------------------------------------
+// Windowed far path (default for p > P_ml): the far primes' hits are routed in
+// two counting-sort levels instead of moving an 8-byte entry from wave bucket
+// to wave bucket at every hit (k_scatter_far).
+//  k_far_walk  once per WINDOW of K waves: walks every far prime through the
+//              window (state = next hit relative to the window start, wheel
+//              class, cofactor mod 7; 8 B read + written per window, not per
+//              hit) and emits one u32 record per hit — its offset inside its
+//              wave — into the record bucket of that wave: the paper's bucket
+//              of the segment of the next hit (large_kernel.hpp:61-213), with
+//              the bucket filled for K waves ahead in one pass.  Staging,
+//              shared-memory counting sort by wave and coalesced runs as in
+//              the ML scatter; emission is compacted (ballot + popc).
+//  k_wave_sort once per wave: partitions the wave's record bucket by tile into
+//              the tiles' hit lists (dense: every lane holds a record).
+struct FarWalkArgs {
+  const uint32_t* primes;  // the far primes (ascending)
+  uint64_t* st;            // per far prime: pos (40 bits) | s << 40 | c7 << 43
+  uint32_t nfar;
+  uint64_t lim;   // valid bits of this window (walk bound)
+  uint64_t span;  // K * WS: the state is re-based by this after the window
+  uint32_t WS, log_s, magic;  // wave of tile t in the window = umulhi(t, magic)
+  uint32_t nbins;             // waves of this window
+  uint32_t* wbuf;             // [K][wcap] + trash
+  uint32_t* wcnt;             // [K]
+  uint32_t wcap, trash_at;    // trash_at = K * wcap
+  int* overflow;
+};
+
+// test-only fault (ERATO_GPU_TEST_INJECT=2): a record outside its wave
+__global__ void k_inject_wrec(uint32_t* wbuf, const uint32_t* wcnt) {
+  if (*wcnt) wbuf[0] |= 0x80000000u;
+}
+
+constexpr uint64_t kFarPosMask = (1ull << 40) - 1;
+__device__ __forceinline__ uint64_t farw_pack(uint64_t pos, uint32_t s, uint32_t c7) {
+  return (pos & kFarPosMask) | ((uint64_t)(s & 7) << 40) | ((uint64_t)c7 << 43);
+}
+
+#ifndef EG_WK_WARPS
+#define EG_WK_WARPS 8
+#endif
+#ifndef EG_WK_STEPS
+#define EG_WK_STEPS 12
+#endif
+constexpr int kWkWarps = EG_WK_WARPS, kWkSteps = EG_WK_STEPS;
+
+struct WkSmem {
+  static constexpr int R = kWkSteps * 32;  // staged records per warp
+  uint32_t val[kWkWarps * R];
+  uint32_t rb[kWkWarps * R];  // rank among the round's records of the same wave | wave << 16
+  uint32_t srt[kWkWarps * R];
+  uint8_t sbin[kWkWarps * R];
+  uint32_t cnt[kScBins], off[kScBins], gofs[kScBins];
+  uint32_t total;
+  static_assert(kWkWarps * R < 65536, "ranks are 16-bit");
+};
+
+// Exclusive scan of cnt[0..nb) into off by warp 0 while the other warps
+// reserve c slots per non-empty bin in gcnt[b]: gofs[b] = global index of the
+// bin's first reserved slot (the caller subtracts off[b] after the barrier).
+template <int NW>
+__device__ __forceinline__ void scan_reserve(const uint32_t* cnt, uint32_t* off, uint32_t* gofs, uint32_t* total,
+                                             uint32_t nb, uint32_t* gcnt, uint32_t cap, uint32_t trash_at,
+                                             int* overflow) {
+  const uint32_t tid = threadIdx.x;
+  if (tid < 32) {
+    const uint32_t tot = warp_excl_scan(cnt, off, nb);
+    if (tid == 0) *total = tot;
+  } else {
+    for (uint32_t b = tid - 32; b < nb; b += NW * 32 - 32) {
+      const uint32_t c = cnt[b];
+      if (c) {
+        const uint32_t r = atomicAdd(&gcnt[b], c);
+        const bool over = r + c > cap;
+        if (over) atomicExch(overflow, 1);
+        gofs[b] = over ? trash_at : b * cap + r;
+      }
+    }
+  }
+}
+
+template <bool FAR7>
+__global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  WkSmem& sm = *reinterpret_cast<WkSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t NT = kWkWarps * 32;
+  for (uint32_t t = tid; t < kScBins; t += NT) sm.cnt[t] = 0;
+  __syncthreads();
+  const uint32_t WS = a.WS, shift = a.log_s, magic = a.magic;
+  const uint64_t lim = a.lim, span = a.span;
+  const uint32_t nw = gridDim.x * kWkWarps;
+  const uint32_t nu = (a.nfar + 31) / 32;
+  uint32_t ltm;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+  const uint32_t val_a = smem_addr(sm.val + warp * WkSmem::R), rb_a = smem_addr(sm.rb + warp * WkSmem::R),
+                 cnt_a = smem_addr(sm.cnt);
+  const uint32_t gw0 = blockIdx.x * kWkWarps + warp;
+  uint32_t urow = 0;
+  auto unit_at = [&](uint32_t k) -> uint32_t { return k * nw + ((EG_BOUS && (k & 1)) ? nw - 1 - gw0 : gw0); };
+  uint32_t u = gw0;
+  uint32_t idx = u * 32 + lane;
+  bool ok = u < nu && idx < a.nfar;
+  uint32_t p = ok ? a.primes[idx] : 0;
+  uint64_t e = ok ? a.st[idx] : ~0ull;
+  uint64_t pos;
+  uint32_t s, c7, dd;
+  auto decode = [&]() {
+    pos = ok ? (e & kFarPosMask) : lim;
+    s = (uint32_t)(e >> 40) & 7;
+    c7 = (uint32_t)(e >> 43) & 7;
+    dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+  };
+  decode();
+  // the next unit's prime and state are in flight
+  uint32_t pn = 0;
+  uint64_t en = 0;
+  auto prefetch = [&](uint32_t uu) {
+    const uint32_t j = uu * 32 + lane;
+    if (uu < nu && j < a.nfar) {
+      pn = a.primes[j];
+      en = a.st[j];
+    }
+  };
+  prefetch(unit_at(1));
+  bool live = u < nu;  // warp-uniform
+  for (;;) {
+    uint32_t kb = 0;  // staged records of this warp (warp-uniform)
+    while (live && kb <= (uint32_t)WkSmem::R - 32) {
+      const bool v = pos < lim;
+      const uint32_t m = __ballot_sync(kFull, v);
+      if (!m) {
+        if (ok) a.st[idx] = farw_pack(pos - span, s, c7);
+        ++urow;
+        u = unit_at(urow);
+        if (u >= nu) {
+          live = false;
+          break;
+        }
+        idx = u * 32 + lane;
+        ok = idx < a.nfar;
+        p = pn;
+        e = en;
+        decode();
+        prefetch(unit_at(urow + 1));
+        continue;
+      }
+      const uint32_t slot = kb + __popc(m & ltm);
+      kb += __popc(m);
+      if (v) {
+        const uint32_t tile = (uint32_t)(pos >> shift);
+        const uint32_t wv = __umulhi(tile, magic);
+        const uint32_t off = (uint32_t)pos - wv * WS;
+        EG_CHECK(wv < a.nbins && off < WS, "far walk wave=%u nbins=%u off=%u", wv, a.nbins, off);
+        uint32_t r;
+        asm volatile(
+            "atom.shared.add.u32 %0, [%1], 1;\n\t"
+            "st.shared.u32 [%2], %3;"
+            : "=r"(r)
+            : "r"(cnt_a + (wv << 2)), "r"(val_a + (slot << 2)), "r"(off)
+            : "memory");
+        uint32_t D = dd & 15u;
+        dd = rotr4(dd);
+        ++s;
+        if (FAR7) {  // the next admissible cofactor may be divisible by 7: then take the one after
+          c7 += 2 * D;
+          c7 -= c7 >= 7 ? 7 : 0;
+          if (c7 == 0) {
+            const uint32_t D2 = dd & 15u;
+            D += D2;
+            dd = rotr4(dd);
+            ++s;
+            c7 = 2 * D2;
+          }
+        }
+        pos += (uint64_t)D * p;
+        sts_u32(rb_a + (slot << 2), r | (wv << 16));
+      }
+    }
+    const int more = __syncthreads_or(live);
+    // ---- round: sort this round's records by wave, coalesced runs out ----
+    scan_reserve<kWkWarps>(sm.cnt, sm.off, sm.gofs, &sm.total, a.nbins, a.wcnt, a.wcap, a.trash_at, a.overflow);
+    __syncthreads();
+    {
+      const uint32_t off_a = smem_addr(sm.off), srt_a = smem_addr(sm.srt), sbin_a = smem_addr(sm.sbin);
+#pragma unroll 2
+      for (uint32_t i = lane; i < kb; i += 32) {
+        const uint32_t rb = lds_u32(rb_a + 4 * i), b = rb >> 16;
+        const uint32_t k = lds_u32(off_a + 4 * b) + (rb & 0xffffu);
+        sts_u32(srt_a + 4 * k, lds_u32(val_a + 4 * i));
+        asm volatile("st.shared.u8 [%0], %1;" : : "r"(sbin_a + k), "r"(b) : "memory");
+      }
+    }
+    for (uint32_t b = tid; b < a.nbins; b += NT) {
+      if (sm.cnt[b]) sm.gofs[b] -= sm.off[b];
+      sm.cnt[b] = 0;
+    }
+    __syncthreads();
+    const uint32_t total = sm.total;
+    for (uint32_t i = tid; i < total; i += NT) a.wbuf[sm.gofs[sm.sbin[i]] + i] = sm.srt[i];
+    // off/gofs/srt are rewritten only after the next round's first barrier
+    if (!more) break;
+  }
+}
+
+// Partition of one wave's far records by tile into the tiles' hit lists.
+constexpr int kWsSegs = 9;  // record segments one launch sorts: the far bucket of the wave + the ML sub-buckets
+struct WaveSortArgs {
+  const uint32_t* in[kWsSegs];        // record segments (offsets inside the wave), blockIdx.y picks one
+  const uint32_t* in_count[kWsSegs];
+  uint32_t cap[kWsSegs];
+  uint32_t nb, log_s;        // tiles of this wave
+  uint32_t* hits;            // [nb][hcap] + trash
+  uint32_t* hitcnt;          // [nb]
+  uint32_t hcap;
+  int* overflow;
+};
+constexpr int kWsThreads = 512, kWsPer = 8, kWsChunk = kWsThreads * kWsPer;
+struct WsSmem {
+  uint32_t srt[kWsChunk];
+  uint32_t cnt[kScBins], off[kScBins], gofs[kScBins];
+  uint32_t total;
+};
+
+// One chunk of kWsChunk records per CTA (the grid covers the bucket's
+// capacity; CTAs past the count exit).  The kernel is latency-bound, so the
+// scan runs on all warps (32 bins each, a warp sums the lower groups itself).
+__global__ void __launch_bounds__(kWsThreads) k_wave_sort(const WaveSortArgs a) {
+  __shared__ WsSmem sm;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t n = min(*a.in_count[blockIdx.y], a.cap[blockIdx.y]);
+  const uint32_t c0 = blockIdx.x * kWsChunk;
+  if (c0 >= n) return;
+  const uint32_t* const in = a.in[blockIdx.y];
+  const uint32_t nb = a.nb, shift = a.log_s, smask = (1u << shift) - 1;
+  const uint32_t cnt_a = smem_addr(sm.cnt), off_a = smem_addr(sm.off), srt_a = smem_addr(sm.srt),
+                 gofs_a = smem_addr(sm.gofs);
+  constexpr int K4 = kWsPer / 4;
+  uint32_t key[kWsPer], rk[kWsPer];
+#pragma unroll
+  for (int k = 0; k < K4; ++k) {
+    const uint32_t i = c0 + 4 * (tid + k * kWsThreads);
+    uint4 v = make_uint4(kNoRec, kNoRec, kNoRec, kNoRec);
+    if (i + 3 < n) {
+      v = __ldcs(reinterpret_cast<const uint4*>(in + i));
+    } else {
+      if (i < n) v.x = in[i];
+      if (i + 1 < n) v.y = in[i + 1];
+      if (i + 2 < n) v.z = in[i + 2];
+    }
+    key[4 * k] = v.x;
+    key[4 * k + 1] = v.y;
+    key[4 * k + 2] = v.z;
+    key[4 * k + 3] = v.w;
+  }
+  for (uint32_t t = tid; t < kScBins; t += kWsThreads) sm.cnt[t] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kWsPer; ++k) {
+    const uint32_t t = key[k] >> shift;
+    rk[k] = 0;
+    if (t < nb) {  // (sentinels and corrupted records are dropped)
+      asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(rk[k]) : "r"(cnt_a + (t << 2)) : "memory");
+    }
+  }
+  __syncthreads();
+  for (uint32_t w = warp; w * 32 < nb; w += kWsThreads / 32) {
+    const uint32_t b = w * 32 + lane;
+    const uint32_t c = b < nb ? sm.cnt[b] : 0;
+    uint32_t low = 0;
+    for (uint32_t j = 0; j < w; ++j) low += sm.cnt[j * 32 + lane];
+    uint32_t r = 0;
+    bool over = false;
+    if (c) {
+      r = atomicAdd(&a.hitcnt[b], c);
+      over = r + c > a.hcap;
+      if (over) atomicExch(a.overflow, 1);
+    }
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) low += __shfl_xor_sync(kFull, low, o);
+    const uint32_t ofs = low + x - c;
+    if (b < nb) {
+      sm.off[b] = ofs;
+      if (c) sm.gofs[b] = (over ? nb * a.hcap : b * a.hcap + r) - ofs;  // global index of sorted slot 0 of the tile
+      if (b == nb - 1) sm.total = ofs + c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kWsPer; ++k) {
+    const uint32_t t = key[k] >> shift;
+    if (t < nb) sts_u32(srt_a + 4 * (lds_u32(off_a + 4 * t) + rk[k]), key[k]);
+  }
+  __syncthreads();
+  const uint32_t total = sm.total;
+  for (uint32_t i = tid; i < total; i += kWsThreads) {
+    const uint32_t k = lds_u32(srt_a + 4 * i);
+    a.hits[lds_u32(gofs_a + 4 * (k >> shift)) + i] = k & smask;
+  }
+}
+
+static_assert(kWkWarps * WkSmem::R <= (int)kScTrash && kWsChunk <= (int)kScTrash, "trash area too small");
+
+// invariant check of a wave's far records (ERATO_GPU_CHECK_INVARIANTS): each
+// lies inside the wave's tiles
+__global__ void __launch_bounds__(256) k_check_wrecs(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_count,
+                                                     uint32_t wcap, uint32_t lim, int* bad) {
+  const uint32_t n = min(*in_count, wcap);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    if (in[j] >= lim) atomicExch(bad, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1658,6 +2191,7 @@ struct SetupArgs {
   int inject;  // test-only fault injection on the first far prime: 1 drop its entry, 2 corrupt its q
   int far7;    // far entries in the mod-210 format (far7_pack)
   int ml7;     // ML states in the mod-210 format (ml7_pack)
+  uint64_t* fst;  // windowed far path: per far prime state (farw_pack) instead of bucket entries
 };
 
 constexpr int kSetupThreads = 1024;
@@ -1701,11 +2235,15 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
           s = (s + 1) & 7;
         }
       }
+      if (a.fst) {  // first hit relative to the run start (= start of window 0)
+        if (a.inject == 1 && i == a.i_ml_end) pos = kFarPosMask;  // test-only: the prime never hits
+        a.fst[i - a.i_ml_end] = farw_pack(pos, s, a.far7 ? c7 : 1);
+      }
       // d = pos / WS: fp64 estimate (pos < 2^40, off by at most one), exact fix
       uint64_t d = __double2ull_rz(__dmul_rz(__ull2double_rz(pos), a.inv_ws));
       if (d * a.WS > pos) --d;
       if ((d + 1) * a.WS <= pos) ++d;
-      if (d < a.nwaves) {
+      if (!a.fst && d < a.nwaves) {
         app = true;
         slotb = (uint32_t)d % a.ring;
         const uint32_t q = (uint32_t)(pos - d * a.WS);

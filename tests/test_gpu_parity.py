@@ -455,6 +455,36 @@ def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
         assert results[2][2] < results[0][2]
 
 
+@pytest.mark.parametrize("l,f,n", [(22, (1 << 37) - 4096, 700), (21, (1 << 26) - 2048, 300), (20, 1 << 21, 60),
+                                   (22, (1 << 37) - 4096, 37)])
+def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
+    """The default large-prime pipeline — unsorted ML records (k_ml_emit), the
+    windowed far walk (k_far_walk), one partition by tile per wave
+    (k_wave_sort) — gives the same table as every older path it replaced: the
+    sorting ML scatter, the per-wave far bucket ring, a far class starting
+    below the wave span, several windows per run."""
+    import paper_1111_3297_b200 as E
+    p = E.validate_params(l, f, n)
+    keys = ("ERATO_GPU_FAR", "ERATO_GPU_ML", "ERATO_GPU_FAR_DIV", "ERATO_GPU_FAR_WINDOW")
+    results = []
+    for env in ({}, {"ERATO_GPU_FAR": "ring"}, {"ERATO_GPU_ML": "emit"},
+                {"ERATO_GPU_FAR": "ring", "ERATO_GPU_ML": "emit"},
+                {"ERATO_GPU_FAR_DIV": "4", "ERATO_GPU_FAR_WINDOW": "2"}, {"ERATO_GPU_FAR_WINDOW": "1"}):
+        old = {k: os.environ.get(k) for k in keys}
+        os.environ.update(env)
+        try:
+            st = gpu_ctx.count(p, check_invariants=True)
+            t, _ = gpu_ctx.table(p)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        results.append((st.prime_count, sha(t)))
+    assert len(set(results)) == 1, results
+
+
 @pytest.mark.parametrize("limit", [4096, 92681, 1049087, 16777471, 1073741839])
 def test_base_prime_list_equals_reference_simple_sieve(reference, limit):
     """The device base-prime list (odd primes <= isqrt(v) of cfg1..cfg5),
