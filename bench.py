@@ -58,13 +58,10 @@ ROOF = {
     4: (19_421_366_720, 7_608_331_782),
     5: (174_787_646_624, 37_185_502_020),
 }
-# This implementation's own work (tools/roofline_counts.py `ours_*`, 2^20-bit
-# tiles, 148-tile waves): hit records of the ML primes (S < p <= wave span) and
-# of the far primes, each as (mod-30 wheel, mod 210: cofactors divisible by 7
-# skipped — stats.skip7 says which a run used), and medium-prime marks.
+# This implementation's own medium-prime marks (tools/roofline_counts.py `ours_*`, 2^20-bit tiles);
+# the large-prime hit records are counted on the device by the run itself (stats.large_records /
+# far_records with ERATO_GPU_CHECK_INVARIANTS) — they depend on the wheel modulus and the ML/far split.
 # (cfg3's 37 primes just above the tile size are sieved as medium primes: no records)
-ML_RECORDS = {1: (0, 0), 2: (0, 0), 3: (0, 0), 4: (835_065_655, 715_771_037), 5: (5_640_109_053, 4_834_378_943)}
-FAR_RECORDS = {1: (0, 0), 2: (0, 0), 3: (0, 0), 4: (0, 0), 5: (1_789_110_090, 1_533_518_655)}
 MEDIUM_MARKS = {1: 2_704_493, 2: 2_151_023_657, 3: 673_975_296, 4: 5_391_802_774, 5: 21_567_210_790}
 METRIC = "sieved numbers/sec at 2^48 & 2^60 midpoints, 1/2/4/8 GPU; % of HBM roofline"
 # smem atomicOr/s per B200 at random word addresses (the sieve's bank-conflict
@@ -278,10 +275,12 @@ def measure(R: Rank, cfg: int, steps: int, warmup: int):
     # per-kernel phase split: one extra pass with CUDA events around every launch
     R.flush_buf.fill_(1)
     ph = step(flags_extra=0x100)
+    # the run's own record counts: one pass with the device invariant checks on (untimed)
+    inv = step(flags_extra=0x200)
     del table
     return {"cfg": cfg, "params": params, "times": times, "t_max": t_max, "count": total_count, "numbers": numbers,
             "value": numbers * steps / t_max, "ms": t_max / steps * 1e3, "launches": launches, "phase": ph,
-            "clocks": clk.summary()}
+            "records": (inv.large_records, inv.far_records), "clocks": clk.summary()}
 
 
 def roofline(m, world: int):
@@ -305,25 +304,33 @@ def roofline(m, world: int):
         "atomic_rate_peak": R_ATOM_MEASURED,
         "t_roof_ms": round(max(t_hbm, t_atom) * 1e3 / world, 3),
         "frac_of_roofline": round(max(t_hbm, t_atom) / world / secs, 4),
-        "kernel_split_ms": {"k_tile": round(ph.small_s * 1e3, 3), "k_scatter_ml": round(ph.gen_s * 1e3, 3),
-                            "k_scatter_far": round(ph.bin_s * 1e3, 3), "init": round(ph.init_s * 1e3, 3),
+        "kernel_split_ms": {"k_tile": round(ph.small_s * 1e3, 3), "k_ml_walk": round(ph.gen_s * 1e3, 3),
+                            "k_far_walk": round(ph.walk_s * 1e3, 3),
+                            "k_wave_sort": round((ph.bin_s - ph.walk_s) * 1e3, 3), "init": round(ph.init_s * 1e3, 3),
                             "masks_phase_cta0": round(ph.masks_s * 1e3, 3)},
+        "large_prime_wheel": ph.wheel,
     }
     # ---- per-kernel: algorithmic bytes per launch / average launch time ----
+    # record counts of THIS run (device-counted with ERATO_GPU_CHECK_INVARIANTS
+    # in an untimed pass): all large-prime hit records, and the far primes' share
     waves = max(ph.waves, 1)
-    far = FAR_RECORDS[cfg][1 if ph.skip7 & 1 else 0] / world
-    ml = ML_RECORDS[cfg][1 if ph.skip7 & 2 else 0] / world
-    recs = ml + far
+    recs, far = m["records"]
+    ml = recs - far
+    nwin = max(ph.far_windows, 1)
     table_bytes = m["params"].table_bytes()
     alg = {
         # table written once + every hit record read once
         "k_tile": (table_bytes + 4.0 * recs) / waves,
-        # ML records written + every ML state read and rewritten (8 B + 8 B) each wave
-        "k_scatter_ml": 4.0 * ml / waves + 16.0 * ph.ml_primes,
-        # per far entry visited: 8 B entry in, 8 B re-bucketed entry out, 4 B record out
-        "k_scatter_far": 20.0 * far / waves,
+        # per wave: ML records written + every ML prime read (4 B) and its state read and rewritten (8 B + 8 B)
+        "k_ml_walk": 4.0 * ml / waves + 20.0 * ph.ml_primes,
+        # per window of waves: far records written + every far prime read (4 B), state read and rewritten (8 B + 8 B)
+        "k_far_walk": 4.0 * far / nwin + 20.0 * ph.far_primes,
+        # per wave: the wave's far records read and written once
+        "k_wave_sort": 8.0 * far / waves,
     }
-    launch_s = {"k_tile": ph.small_s / waves, "k_scatter_ml": ph.gen_s / waves, "k_scatter_far": ph.bin_s / waves}
+    launch_s = {"k_tile": ph.small_s / waves, "k_ml_walk": ph.gen_s / waves, "k_far_walk": ph.walk_s / nwin,
+                "k_wave_sort": (ph.bin_s - ph.walk_s) / waves}
+    step_s = {"k_tile": ph.small_s, "k_ml_walk": ph.gen_s, "k_far_walk": ph.walk_s, "k_wave_sort": ph.bin_s - ph.walk_s}
     traffic, tsrc = ncu_traffic(cfg)
     kernels = {}
     for k in alg:
@@ -334,11 +341,12 @@ def roofline(m, world: int):
                       "achieved": round(ach, 1), "frac": round(ach / hbm, 4),
                       "traffic": (traffic or {}).get(k)}
     tile_atoms = MEDIUM_MARKS[cfg] / world / waves + recs / waves
+    run["large_prime_records"] = {"all": recs, "far": far}
     if launch_s["k_tile"] > 0:
         kernels["k_tile"]["smem_atomics_per_launch"] = round(tile_atoms)
         kernels["k_tile"]["atomic_rate"] = round(tile_atoms / launch_s["k_tile"], 1)
         kernels["k_tile"]["atomic_frac"] = round(tile_atoms / launch_s["k_tile"] / R_ATOM_MEASURED, 4)
-    dom = max(launch_s, key=launch_s.get)
+    dom = max(step_s, key=step_s.get)  # the kernel with the largest share of the step
     d = kernels.get(dom, {})
     roof = {"bound": "hbm", "kernel": dom, "achieved": d.get("achieved", 0.0), "peak": hbm, "unit": "GB/s",
             "frac": d.get("frac", 0.0), "traffic": d.get("traffic"),

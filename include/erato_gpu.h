@@ -80,16 +80,21 @@ typedef struct {
   uint32_t waves;
   uint32_t kernel_launches;
   uint32_t retries; /* capacity re-runs after a bucket overflow */
-  double gen_s;     /* with ERATO_GPU_PHASE_TIMING: ML scatter (k_scatter_ml; k_gen on the fallback) */
-  double bin_s;     /* with ERATO_GPU_PHASE_TIMING: far scatter (k_scatter_far; k_bin on the fallback) */
+  double gen_s;     /* with ERATO_GPU_PHASE_TIMING: ML walk per wave (k_ml_walk; k_scatter_ml / k_gen on the legacy paths) */
+  double bin_s;     /* with ERATO_GPU_PHASE_TIMING: far primes (k_far_walk per window + k_wave_sort per wave;
+                       k_scatter_far / k_bin on the legacy paths) */
   uint64_t large_records; /* with ERATO_GPU_CHECK_INVARIANTS: hit records consumed by the tiles */
   double masks_s; /* with ERATO_GPU_PHASE_TIMING: the small-prime pattern phase of the tile kernel
                      (apply_small_masks, driver.cpp:97-99), %globaltimer in CTA 0 of each launch */
   uint64_t medium_primes; /* base primes sieved inside the tiles (61 < p <= tile) */
   uint64_t ml_primes;     /* large primes walked every wave (tile < p <= wave span) */
-  uint64_t far_primes;    /* large primes kept in the per-wave bucket ring (p > wave span) */
-  uint32_t skip7;         /* bit 0: far primes, bit 1: ML primes skip cofactors divisible by 7 (mod 210) */
-  uint32_t reserved0;
+  uint64_t far_primes;    /* large primes walked once per window of waves (p > wave span / far_div) */
+  uint32_t skip7;         /* bit 0: far primes, bit 1: ML primes skip cofactors divisible by 7 */
+  uint32_t wheel;         /* wheel modulus of the large primes (30, 210, 2310, 30030); 0 on the legacy paths */
+  uint64_t far_records;   /* with ERATO_GPU_CHECK_INVARIANTS: hit records of the far primes (of large_records) */
+  double walk_s;          /* with ERATO_GPU_PHASE_TIMING: the k_far_walk part of bin_s */
+  uint32_t far_windows;   /* k_far_walk launches (windows of waves) of the run */
+  uint32_t reserved1;
 } erato_gpu_stats;
 
 /* Count written to a caller's dev_count when a bucket / hit-list capacity

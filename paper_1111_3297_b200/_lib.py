@@ -42,7 +42,8 @@ class Stats(C.Structure):
         ("kernel_launches", C.c_uint32), ("retries", C.c_uint32),
         ("gen_s", C.c_double), ("bin_s", C.c_double), ("large_records", C.c_uint64),
         ("masks_s", C.c_double), ("medium_primes", C.c_uint64), ("ml_primes", C.c_uint64),
-        ("far_primes", C.c_uint64), ("skip7", C.c_uint32), ("reserved0", C.c_uint32),
+        ("far_primes", C.c_uint64), ("skip7", C.c_uint32), ("wheel", C.c_uint32),
+        ("far_records", C.c_uint64), ("walk_s", C.c_double), ("far_windows", C.c_uint32), ("reserved1", C.c_uint32),
     ]
 
 

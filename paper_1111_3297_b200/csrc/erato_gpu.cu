@@ -109,7 +109,9 @@ struct erato_gpu_ctx {
   DevBuf base_bits, primes, med, ml, buckets, bcount, hits, hitcnt, blk_cnt, blk_off, scal, table, outbuf;
   DevBuf recs, rcount, frecs, fslot, fcount;  // k_gen -> k_bin per-warp regions
   DevBuf fst, wbuf, wcnt;                     // windowed far path: prime states, per-wave record buckets
-  DevBuf mlrec, mlcnt;                        // k_ml_emit: unsorted ML records of the wave, kMlSub buckets
+  DevBuf mlst;                                // wheel mode: ML states (pos | idx << 32)
+  DevBuf wdelta, wrank;                       // wheel tables of the large primes (cached per modulus)
+  uint32_t wheel_M = 0, wheel_nres = 0;
   double hcap_scale = 1.0, bcap_scale = 1.0;
   uint64_t max_base_pairs = uint64_t{1} << 27;  // base.hpp:87
   cudaEvent_t ev[4] = {};
@@ -278,8 +280,10 @@ int create_impl(erato_gpu_ctx* c) {
     CUDA_TRY(cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::MlSmem)));
   for (auto kf : {eg::k_scatter_far<false>, eg::k_scatter_far<true>})
     CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::FarSmem)));
-  for (auto kw : {eg::k_far_walk<false>, eg::k_far_walk<true>})
-    CUDA_TRY(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(eg::WkSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_far_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(eg::WkSmem) + 16 + eg::kWheelMaxBytes)));
+  CUDA_TRY(cudaFuncSetAttribute(eg::k_ml_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(eg::MlSmem) + 16 + eg::kWheelMaxBytes)));
   // cached tables: small primes < 2^16 and the pattern windows
   CUDA_TRY(c->sp.ensure(8192 * 4));
   CUDA_TRY(c->spm.ensure((8192 + eg::kMedPad) * 16));
@@ -327,7 +331,7 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
                     &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount, &c->slices, &c->fst,
-                    &c->wbuf, &c->wcnt, &c->mlrec, &c->mlcnt})
+                    &c->wbuf, &c->wcnt, &c->mlst, &c->wdelta, &c->wrank})
     b->release();
   if (c->hslots) cudaFreeHost(c->hslots);
   if (c->hflags) cudaFreeHost(c->hflags);
@@ -437,6 +441,35 @@ int base_primes(erato_gpu_ctx* c, cudaStream_t st, uint64_t vroot, uint32_t& lau
                                          c->primes.as<uint32_t>(), prime_cap, d_scal + 0);
   if (rc) return rc;
   launches += 3;
+  return 0;
+}
+
+// Wheel tables of the large primes for modulus M (30, 210, 2310 or 30030):
+// delta[i] = half the gap from the i-th residue coprime to M to the next one
+// (wrapping), rank[r] = index of residue r (0xffff if not coprime).  Cached.
+int ensure_wheel(erato_gpu_ctx* c, cudaStream_t st, uint32_t M) {
+  if (c->wheel_M == M) return 0;
+  std::vector<uint32_t> res;
+  std::vector<uint16_t> rank(M, 0xffff);
+  for (uint32_t r = 1; r < M; r += 2)
+    if (r % 3 && r % 5 && (M % 7 || r % 7) && (M % 11 || r % 11) && (M % 13 || r % 13)) {
+      rank[r] = (uint16_t)res.size();
+      res.push_back(r);
+    }
+  if (res.size() > eg::kWheelMaxRes || res.size() % 8) return fail(ERATO_GPU_E_INVALID_ARG, "wheel size");
+  std::vector<uint32_t> delta(res.size() / 8 + 1, 0);  // 8 nibbles per word + the wrap-around word
+  for (size_t i = 0; i < res.size(); ++i) {
+    const uint32_t nxt = i + 1 < res.size() ? res[i + 1] : res[0] + M;
+    delta[i / 8] |= ((nxt - res[i]) / 2) << (4 * (i % 8));  // half gaps <= 11
+  }
+  delta.back() = delta[0];
+  CUDA_TRY(c->wdelta.ensure(eg::kWheelMaxBytes));
+  CUDA_TRY(c->wrank.ensure((size_t)30030 * 2));
+  CUDA_TRY(cudaMemcpyAsync(c->wdelta.p, delta.data(), delta.size() * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->wrank.p, rank.data(), rank.size() * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));  // (the host vectors go out of scope)
+  c->wheel_M = M;
+  c->wheel_nres = (uint32_t)res.size();
   return 0;
 }
 
@@ -606,18 +639,32 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
   P.WS = P.W * P.S;
   P.nwaves = (P.ntiles + P.W - 1) / P.W;
   P.MW = 1;  // (an ML walk over 2 waves per launch measured 2 ms slower at cfg5)
-  // Far primes: the windowed two-level path (k_far_walk + k_wave_sort) unless
-  // ERATO_GPU_FAR=ring asks for the per-wave bucket ring (k_scatter_far) or
-  // the k_gen/k_bin fallback is forced.  In window mode the far class starts
-  // at WS / far_div: ML primes that hit a wave less than ~far_div/2 times
-  // cost more per record in the per-wave walk than through the two levels.
+  // Large primes, default ("wheel") path: table-driven wheel walks — ML primes
+  // per wave (k_ml_walk), far primes per window of waves (k_far_walk) with one
+  // partition by tile per wave (k_wave_sort).  ERATO_GPU_LARGE=legacy selects
+  // the round-1/2 structures instead (mod-30/210 states, k_scatter_ml, the far
+  // bucket ring k_scatter_far, or k_gen/k_bin with ERATO_GPU_SCATTER=genbin).
+  // In wheel mode the far class starts at WS / far_div.
   const char* sc_env0 = std::getenv("ERATO_GPU_SCATTER");
-  const char* fm_env = std::getenv("ERATO_GPU_FAR");
-  const bool win = !(fm_env && std::strcmp(fm_env, "ring") == 0) && !(sc_env0 && std::strcmp(sc_env0, "genbin") == 0) &&
+  const char* lg_env = std::getenv("ERATO_GPU_LARGE");
+  const bool win = !(lg_env && std::strcmp(lg_env, "legacy") == 0) && !(sc_env0 && std::strcmp(sc_env0, "genbin") == 0) &&
                    P.W <= (uint32_t)eg::kScBins;
-  uint32_t far_div = 1;
+  uint32_t wheel_M = 30030;
+  if (const char* e = std::getenv("ERATO_GPU_WHEEL")) wheel_M = (uint32_t)std::atoi(e);
+  if (wheel_M != 30 && wheel_M != 210 && wheel_M != 2310 && wheel_M != 30030)
+    return fail(ERATO_GPU_E_INVALID_ARG, "ERATO_GPU_WHEEL must be 30, 210, 2310 or 30030");
+  const uint32_t wmask = (wheel_M % 7 == 0 ? 1u : 0u) | (wheel_M % 11 == 0 ? 2u : 0u) | (wheel_M % 13 == 0 ? 4u : 0u);
+  const double wdens = (8.0 / 15.0) * ((wmask & 1) ? 6.0 / 7.0 : 1.0) * ((wmask & 2) ? 10.0 / 11.0 : 1.0) *
+                       ((wmask & 4) ? 12.0 / 13.0 : 1.0);  // records per odd multiple
+  if (win) {
+    rc = ensure_wheel(c, st, wheel_M);
+    if (rc) return rc;
+  }
+  // (cfg5, same-box A/B: far_div 1 / 2 / 4 / 8 = 54.1 / 51.4 / 49.9 / 50.1 ms — an ML prime above WS/4 hits a
+  // wave less than twice, and the per-wave walk pays a state round trip and 2-3 mostly idle steps for it)
+  uint32_t far_div = 4;
   if (const char* e = std::getenv("ERATO_GPU_FAR_DIV")) far_div = (uint32_t)std::max(1, std::atoi(e));
-  uint32_t kwin_max = 64;
+  uint32_t kwin_max = 128;
   if (const char* e = std::getenv("ERATO_GPU_FAR_WINDOW")) kwin_max = (uint32_t)std::max(1, std::atoi(e));
   kwin_max = std::min<uint32_t>(kwin_max, eg::kScBins);
 
@@ -632,6 +679,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     uint64_t* d_scal = c->scal.as<uint64_t>();
     CUDA_TRY(cudaMemsetAsync(d_scal + 18, 0, 16, st));
     CUDA_TRY(cudaMemsetAsync(d_scal + 21, 0, 8, st));
+    CUDA_TRY(cudaMemsetAsync(d_scal + 23, 0, 8, st));  // [23] far records (CHECK_INVARIANTS)
     rc = base_primes(c, st, vroot, launches);
     if (rc) return rc;
     // ---------------- 3. class boundaries (one host sync) ----------------
@@ -668,7 +716,6 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     const bool have_large = nml + nfar > 0;
     uint32_t ring = 1, bcap = 1, hcap = 4, rcap = 1, fcap = 1;
     uint32_t kwin = 1, wcap = 4, wmagic = 0;  // window mode: waves per window, records per wave bucket
-    uint32_t mlcap = 4;                       // k_ml_emit: records per ML record bucket
     bool split = false, far7 = false, ml7 = false;
     if (have_large) {
       const double lnP = std::log((double)std::max<uint32_t>(pmax, 3));
@@ -677,31 +724,23 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       hcap = (uint32_t)std::min<double>(((eh * 1.10 + 4096) * c->hcap_scale), (double)P.S * 4);
       hcap = (hcap + 3) & ~3u;
       CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
-      {
-        // k_ml_emit record buckets: expected ML records per wave / kMlSub (+15 % and slack)
-        const double sr_ml = std::max(0.0, std::log(std::log((double)std::max<uint64_t>(std::min<uint64_t>(p_ml, pmax), P.S + 1)) /
-                                                    std::log((double)P.S))) + 0.02;
-        const double em = (double)P.WS * (8.0 / 15.0) * sr_ml / eg::kMlSub;
-        mlcap = (uint32_t)std::min<double>((em * 1.15 + 8192) * c->hcap_scale, 1u << 28);
-        mlcap = (mlcap + 3) & ~3u;
-        CUDA_TRY(c->mlrec.ensure(((uint64_t)eg::kMlSub * mlcap + eg::kScTrash) * 4));
-        CUDA_TRY(c->mlcnt.ensure(eg::kMlSub * 4));
-        CUDA_TRY(cudaMemsetAsync(c->mlcnt.p, 0, eg::kMlSub * 4, st));
-      }
+      if (win) CUDA_TRY(c->mlst.ensure(std::max<uint64_t>(nml, 1) * 8));
       // the lists of the MW waves of an ML window, + trash of the split scatter
       CUDA_TRY(c->hits.ensure(((uint64_t)P.MW * P.W * hcap + eg::kScTrash) * 4));
       CUDA_TRY(c->hitcnt.ensure((uint64_t)P.MW * P.W * 4));
       CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.MW * P.W * 4, st));
       if (nfar && win) {
-        const char* f7 = std::getenv("ERATO_GPU_FAR7");
-        const bool w7 = !(f7 && std::strcmp(f7, "0") == 0);
         const double sr_far = std::max(0.0, std::log(lnP / std::log((double)p_ml))) + 0.01;
-        const double ew = (double)P.WS * (8.0 / 15.0) * (w7 ? 6.0 / 7.0 : 1.0) * sr_far;  // records per wave
+        const double ew = (double)P.WS * wdens * sr_far;  // records per wave
         wcap = (uint32_t)std::min<double>((ew * 1.10 + 8192) * c->bcap_scale, 1u << 30);
         wcap = (wcap + 3) & ~3u;
         const uint64_t nwin = (P.nwaves + kwin_max - 1) / kwin_max;
         kwin = (uint32_t)((P.nwaves + nwin - 1) / nwin);
-        while (kwin > 1 && ((uint64_t)kwin * wcap + eg::kScTrash >= (1ull << 32) || (uint64_t)kwin * wcap * 4 > (6ull << 30)))
+        // (the window's record buckets: at most 6 GiB and a quarter of the device memory that is free now)
+        size_t mem_free = 0, mem_total = 0;
+        CUDA_TRY(cudaMemGetInfo(&mem_free, &mem_total));
+        const uint64_t wbudget = std::min<uint64_t>(6ull << 30, std::max<uint64_t>(mem_free / 4 + c->wbuf.cap, 64ull << 20));
+        while (kwin > 1 && ((uint64_t)kwin * wcap + eg::kScTrash >= (1ull << 32) || (uint64_t)kwin * wcap * 4 > wbudget))
           kwin = (kwin + 1) / 2;
         wmagic = (uint32_t)((1ull << 32) / P.W) + 1;  // umulhi(t, wmagic) = t / W for t * W < 2^32
         CUDA_TRY(c->fst.ensure(nfar * 8));
@@ -738,13 +777,13 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       split = sortable && idx32 && !(sc_env && std::strcmp(sc_env, "genbin") == 0);
       // far primes skip cofactors divisible by 7 (mod-210 entries) when p < 2^31 and q < 2^28 fit
       const char* f7_env = std::getenv("ERATO_GPU_FAR7");
-      far7 = split && nfar && (win || (pmax < (1u << 31) && P.WS <= (1u << 28))) &&
+      far7 = split && !win && nfar && pmax < (1u << 31) && P.WS <= (1u << 28) &&
              !(f7_env && std::strcmp(f7_env, "0") == 0);
       // ML primes too (p < 2^28 and next-hit offsets < 6p < 2^30 need WS <= 170 * 2^20), when they all
       // hit a wave >= ~4 times (p <= WS/8: cfg4 -7% ML time); with primes up to WS (cfg5) the extra
       // data-dependent step in the walk costs more than the skipped records save (+13% measured)
       const char* m7_env = std::getenv("ERATO_GPU_ML7");
-      ml7 = split && nml && P.MW == 1 && P.WS <= 170u * (1u << 20) &&
+      ml7 = split && !win && nml && P.MW == 1 && P.WS <= 170u * (1u << 20) &&
             (m7_env ? std::strcmp(m7_env, "1") == 0 : idense >= iWS);
       CUDA_TRY(c->bcount.ensure((uint64_t)ring * 4 + 4));
       CUDA_TRY(cudaMemsetAsync(c->bcount.p, 0, (uint64_t)ring * 4 + 4, st));
@@ -767,7 +806,13 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       if (const char* inj = std::getenv("ERATO_GPU_TEST_INJECT")) sa.inject = std::atoi(inj);  // tests only
       sa.far7 = far7 ? 1 : 0;
       sa.ml7 = ml7 ? 1 : 0;
-      sa.fst = (win && nfar) ? c->fst.as<uint64_t>() : nullptr;
+      if (win) {
+        sa.fst = c->fst.as<uint64_t>();
+        sa.mlst = c->mlst.as<uint64_t>();
+        sa.wrank = c->wrank.as<uint16_t>();
+        sa.wM = wheel_M;
+        sa.wmask = wmask;
+      }
       const uint64_t nl = nprimes - iS;
       eg::k_setup_large<<<(unsigned)((nl + eg::kSetupThreads - 1) / eg::kSetupThreads), eg::kSetupThreads, 0, st>>>(sa);
       ++launches;
@@ -777,7 +822,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         const uint64_t xh = x_hi > UINT64_MAX ? UINT64_MAX : (uint64_t)x_hi;
         eg::k_expected_records<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(
             c->primes.as<uint32_t>(), iS, nprimes, P.u, xh, reinterpret_cast<unsigned long long*>(d_scal + 19),
-            ml7 ? iS : (far7 ? iWS : nprimes), far7 ? nprimes : iWS);
+            win ? iS : (ml7 ? iS : (far7 ? iWS : nprimes)), win ? nprimes : (far7 ? nprimes : iWS), win ? wmask : 1u);
         ++launches;
       }
     } else {
@@ -875,34 +920,31 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     eg::ScatterArgs sca{};
     uint32_t ml_blocks = c->nsm, far_blocks = c->nsm, walk_blocks = c->nsm;
     const bool winfar = win && nfar > 0;
-    const char* ml_env = std::getenv("ERATO_GPU_ML");
-    const bool emit = split && nml > 0 && ml_env && std::strcmp(ml_env, "emit") == 0;  // (measured slower: off by default)
-    uint32_t emit_blocks = c->nsm;
-    eg::MlEmitArgs mea{};
+    const bool wml = win && nml > 0;  // wheel-mode ML walk (k_ml_walk)
+    const size_t wsm_ml = ((sizeof(eg::MlSmem) + 15) & ~size_t{15}) + c->wheel_nres / 2 + 4;
+    const size_t wsm_far = ((sizeof(eg::WkSmem) + 15) & ~size_t{15}) + c->wheel_nres / 2 + 4;
+    eg::Wheel wheel{c->wdelta.as<uint32_t>(), c->wheel_nres};
+    uint32_t mlw_blocks = c->nsm;
+    eg::MlWalkArgs mwa{};
     eg::FarWalkArgs fwa{};
     eg::WaveSortArgs wsa{};
     wsa.log_s = P.log_s;
     wsa.hcap = hcap;
     wsa.overflow = reinterpret_cast<int*>(d_scal + 17);
-    if (emit) {
+    if (wml) {
       int occ = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_ml_emit<false>, eg::kEmWarps * 32, 0));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_ml_walk, eg::kMlWarps * 32, wsm_ml));
       const uint64_t units = (nml + 31) / 32;
-      emit_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
-                                                 std::max<uint64_t>(1, (units + eg::kEmWarps - 1) / eg::kEmWarps));
-      mea.ml = c->ml.as<uint2>();
-      mea.nml = (uint32_t)nml;
-      mea.WS = P.WS;
-      mea.log_s = P.log_s;
-      mea.rec = c->mlrec.as<uint32_t>();
-      mea.cnt = c->mlcnt.as<uint32_t>();
-      mea.cap = mlcap;
-      mea.overflow = wsa.overflow;
+      mlw_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+                                                std::max<uint64_t>(1, (units + eg::kMlWarps - 1) / eg::kMlWarps));
+      mwa.primes = c->primes.as<uint32_t>() + iS;
+      mwa.st = c->mlst.as<uint64_t>();
+      mwa.nml = (uint32_t)nml;
+      mwa.wheel = wheel;
     }
     if (winfar) {
       int occ = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_far_walk<true>, eg::kWkWarps * 32,
-                                                             sizeof(eg::WkSmem)));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_far_walk, eg::kWkWarps * 32, wsm_far));
       const uint64_t units = (nfar + 31) / 32;
       walk_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
                                                  std::max<uint64_t>(1, (units + eg::kWkWarps - 1) / eg::kWkWarps));
@@ -918,6 +960,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       fwa.wcap = wcap;
       fwa.trash_at = kwin * wcap;
       fwa.overflow = reinterpret_cast<int*>(d_scal + 17);
+      fwa.wheel = wheel;
     }
     if (split) {
       int occ = 1;
@@ -949,7 +992,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       sca.hcap = hcap;
       sca.overflow = ga.overflow;
     }
-    const size_t nev = timing ? (size_t)P.nwaves * 5 + 8 : 0;
+    const size_t nev = timing ? (size_t)P.nwaves * 7 + 8 : 0;
     while (c->phase_ev.size() < nev) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
@@ -957,6 +1000,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     }
     size_t evi = 0;
     std::vector<std::pair<size_t, bool>> ev_pairs;  // (first event index, is_scatter)
+    std::vector<size_t> walk_ev;                    // first event index of each k_far_walk launch
     for (uint64_t w = 0; w < P.nwaves; ++w) {
       const uint64_t tile0 = w * P.W;
       const uint32_t ntw = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - tile0);
@@ -975,10 +1019,12 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         ta.hits = hits_w;
         ta.hitcnt = hitcnt_w;
         if (split) {
-          if (emit) {
-            mea.ntiles_w = ntw;
-            if (ml7) eg::k_ml_emit<true><<<emit_blocks, eg::kEmWarps * 32, 0, st>>>(mea);
-            else eg::k_ml_emit<false><<<emit_blocks, eg::kEmWarps * 32, 0, st>>>(mea);
+          if (wml) {
+            mwa.sc = sca;
+            mwa.sc.ntiles_w = ntw;
+            mwa.sc.hits = hits_w;
+            mwa.sc.hitcnt = hitcnt_w;
+            eg::k_ml_walk<<<mlw_blocks, eg::kMlWarps * 32, wsm_ml, st>>>(mwa);
             launches += 1;
           } else if (nml && wi == 0) {  // ML walk over the window's tiles, state re-based by the window span
             eg::ScatterArgs m = sca;
@@ -992,15 +1038,6 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           }
           if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi + 1], st));
           uint32_t nseg = 0, max_cap = 0;  // record segments k_wave_sort partitions by tile
-          if (emit) {
-            for (int k = 0; k < eg::kMlSub; ++k) {
-              wsa.in[nseg] = c->mlrec.as<uint32_t>() + (uint64_t)k * mlcap;
-              wsa.in_count[nseg] = c->mlcnt.as<uint32_t>() + k;
-              wsa.cap[nseg] = mlcap;
-              ++nseg;
-            }
-            max_cap = mlcap;
-          }
           if (winfar) {
             const uint32_t wl = (uint32_t)(w % kwin);
             if (wl == 0) {  // a new window: walk the far primes through its waves
@@ -1008,8 +1045,12 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
               fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
               fwa.lim = std::min<uint64_t>((uint64_t)kwin * P.W, tiles_left) << P.log_s;
               CUDA_TRY(cudaMemsetAsync(c->wcnt.p, 0, (uint64_t)eg::kScBins * 4, st));
-              if (far7) eg::k_far_walk<true><<<walk_blocks, eg::kWkWarps * 32, sizeof(eg::WkSmem), st>>>(fwa);
-              else eg::k_far_walk<false><<<walk_blocks, eg::kWkWarps * 32, sizeof(eg::WkSmem), st>>>(fwa);
+              if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 1], st));
+              eg::k_far_walk<<<walk_blocks, eg::kWkWarps * 32, wsm_far, st>>>(fwa);
+              if (timing) {
+                CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 2], st));
+                walk_ev.push_back(nev - 2 * walk_ev.size() - 1);
+              }
               launches += 1;
               if (w == 0 && sa_inject == 2) eg::k_inject_wrec<<<1, 1, 0, st>>>(fwa.wbuf, fwa.wcnt);  // tests only
             }
@@ -1017,7 +1058,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             const uint32_t* in_count = c->wcnt.as<uint32_t>() + wl;
             if (flags & ERATO_GPU_CHECK_INVARIANTS) {
               eg::k_check_wrecs<<<(unsigned)c->nsm, 256, 0, st>>>(in, in_count, wcap, ntw << P.log_s,
-                                                                  reinterpret_cast<int*>(d_scal + 21));
+                                                                  reinterpret_cast<int*>(d_scal + 21),
+                                                                  reinterpret_cast<unsigned long long*>(d_scal + 23));
               ++launches;
             }
             wsa.in[nseg] = in;
@@ -1060,7 +1102,6 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           evi += 3;
         }
         ta.reset_bucket_count = (nfar && !winfar) ? c->bcount.as<uint32_t>() + slot : nullptr;
-        ta.reset_ml_count = emit ? c->mlcnt.as<uint32_t>() : nullptr;
         if (flags & ERATO_GPU_CHECK_INVARIANTS) {
           eg::k_check_wave<<<(unsigned)c->nsm, 256, 0, st>>>(
               hitcnt_w, ntw, hcap, (nfar && !winfar) ? ga.far_in : nullptr, ga.far_in_count, bcap, P.WS,
@@ -1125,7 +1166,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       }
       return 0;  // overflow cannot be checked without a sync; capacities are generous
     }
-    uint64_t res[7];  // d_scal[16..22]
+    uint64_t res[8];  // d_scal[16..23]
     CUDA_TRY(cudaMemcpyAsync(res, d_scal + 16, sizeof(res), cudaMemcpyDeviceToHost, st));
     const cudaError_t se = cudaStreamSynchronize(st);
     stop_writer();
@@ -1176,6 +1217,13 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         stats->gen_s = tg * 1e-3;
         stats->masks_s = (double)res[6] * 1e-9;
         stats->bin_s = tb * 1e-3;
+        double tw = 0;
+        for (const size_t e0 : walk_ev) {
+          float ms = 0;
+          cudaEventElapsedTime(&ms, c->phase_ev[e0], c->phase_ev[e0 - 1]);
+          tw += ms;
+        }
+        stats->walk_s = tw * 1e-3;
         stats->small_s = ts * 1e-3;
         stats->large_s = tl * 1e-3;
       }
@@ -1183,7 +1231,10 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       stats->medium_primes = nmed;
       stats->ml_primes = nml;
       stats->far_primes = nfar;
-      stats->skip7 = (far7 ? 1u : 0u) | (ml7 ? 2u : 0u);
+      stats->skip7 = win ? ((wmask & 1) ? 3u : 0u) : (far7 ? 1u : 0u) | (ml7 ? 2u : 0u);
+      stats->wheel = win && have_large ? wheel_M : 0;
+      stats->far_records = res[7];
+      stats->far_windows = (win && nfar) ? (uint32_t)((P.nwaves + kwin - 1) / kwin) : 0;
       stats->base_primes = nprimes;
       stats->tiles = P.ntiles;
       stats->log_tile = P.log_s;

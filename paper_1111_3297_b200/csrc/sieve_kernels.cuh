@@ -238,7 +238,6 @@ struct TileArgs {
   uint64_t out_tile0;            //   table + (t - out_tile0) * S/32 (a wave slice when streaming)
   unsigned long long* count;     // zero-bit accumulator
   uint32_t* reset_bucket_count;  // far bucket slot consumed this wave (nullable)
-  uint32_t* reset_ml_count;      // the kMlSub record-bucket counters of k_ml_emit, consumed this wave (nullable)
   unsigned long long* phase_ns;  // nullable: CTA 0 adds its pattern-phase time (masks_s)
 };
 
@@ -574,7 +573,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     if (HITS) a.hitcnt[blockIdx.x] = 0;
     if (blockIdx.x == 0 && a.reset_bucket_count) *a.reset_bucket_count = 0;
   }
-  if (blockIdx.x == 0 && tid < 8 && a.reset_ml_count) a.reset_ml_count[tid] = 0;  // (kMlSub = 8)
 
   // 4. popcount + write-out (count_zeros simd.cpp:18-25, segment_to_bytes
   // driver.cpp:22-27: LSB-first bytes == little-endian words)
@@ -1128,7 +1126,7 @@ struct ScSmem {
   // exclusive scan; gofs[t] = global index of sorted slot 0 of tile t
   // (t*cap + reserved - off)
   uint32_t cnt[kScBins + 32], off[kScBins], gofs[kScBins];
-  uint32_t fcnt[kScBins + 32], fgofs[kScBins];
+  uint32_t fcnt[FAR ? kScBins + 32 : 1], fgofs[FAR ? kScBins : 1];
   uint32_t total;
   static_assert(NW * R < 65536, "ranks are 16-bit");
 };
@@ -1599,123 +1597,137 @@ __global__ void __launch_bounds__(kFarWarps * 32, EG_FAR_MINB) k_scatter_far(con
 }
 
 // ---------------------------------------------------------------------------
-// ML primes, generator only (default): k_ml_emit walks the ML primes exactly
-// like k_scatter_ml but appends the wave's hit records UNSORTED to one of
-// kMlSub record buckets — a warp stages up to R compacted records in shared
-// memory, reserves a run with one global atomicAdd and copies it out in
-// 128-byte rows, without any CTA-wide barrier — and k_wave_sort partitions
-// them by tile together with the wave's far records.  The sort is a dense
-// kernel (every lane holds a record), so splitting generation from
-// partitioning costs fewer instructions per record than sorting each
-// scatter round in the walking CTA.
-constexpr int kMlSub = 8;
-struct MlEmitArgs {
-  uint2* ml;  // ML primes, ascending: {p | s << 29, pos}
-  uint32_t nml;
-  uint32_t WS, ntiles_w, log_s;
-  uint32_t* rec;  // [kMlSub][cap] + trash
-  uint32_t* cnt;  // [kMlSub]
-  uint32_t cap;
-  int* overflow;
+// Wheel tables of the large primes (default path).  A large prime p marks only
+// the multiples c*p whose cofactor c is coprime to the wheel modulus
+// M = 30, 210, 2310 or 30030 (default): every other multiple is divisible by a
+// prime <= 13 and set by the small-prime patterns anyway.  This is the
+// reference's wheel (src/wheel.cpp:10-34: residues coprime to 30, deltas
+// {3,2,1,2,1,2,3,1}) taken three primes further — 5760 residues of 30030,
+// 28 % fewer records than mod 30.  A prime's state is its next hit and the
+// index of that hit's cofactor in the residue list; delta[idx] (half the gap to
+// the next coprime residue, <= 11) * p is the step to the next hit.  The
+// deltas are packed 8 nibbles to a word (+ one wrap-around word); a walking
+// lane keeps the next 8 deltas in a register, so a step costs the reference
+// wheel's shift-and-mask (delta = dd & 15, dd >>= 4, ++idx), and a warp
+// reloads its lanes' windows together every 8th step (warp-uniform, two
+// shared-memory words and a funnel shift per lane).
+constexpr uint32_t kWheelMaxRes = 5760;
+constexpr uint32_t kWheelMaxBytes = kWheelMaxRes / 2 + 4;
+struct Wheel {
+  const uint32_t* delta8;  // [nres / 8 + 1] nibble i of word w = delta[(8w + i) mod nres]
+  uint32_t nres;
 };
-#ifndef EG_EM_WARPS
-#define EG_EM_WARPS 8
-#endif
-#ifndef EG_EM_STEPS
-#define EG_EM_STEPS 12
-#endif
-constexpr int kEmWarps = EG_EM_WARPS, kEmR = EG_EM_STEPS * 32;
+__device__ __forceinline__ void stage_wheel(uint32_t* dst, const Wheel& w) {
+  for (uint32_t i = threadIdx.x; i <= w.nres / 8; i += blockDim.x) dst[i] = w.delta8[i];
+}
+// the 8 deltas from index wi on (wi < nres + 8 is wrapped first)
+__device__ __forceinline__ uint32_t wheel_window(uint32_t wd_a, uint32_t nres, uint32_t& wi) {
+  wi -= wi >= nres ? nres : 0;
+  EG_CHECK(wi < nres, "wheel index %u of %u", wi, nres);
+  const uint32_t a = wd_a + ((wi >> 3) << 2);
+  return __funnelshift_r(lds_u32(a), lds_u32(a + 4), (wi & 7) << 2);
+}
 
-template <bool ML7>
-__global__ void __launch_bounds__(kEmWarps * 32) k_ml_emit(const MlEmitArgs a) {
-  __shared__ uint32_t s_stage[kEmWarps][kEmR];
+// ML primes (S < p <= P_ml), wheel mode: the per-wave walk of k_scatter_ml with
+// the state split in two arrays — the prime list itself (read only) and
+// u64 states pos | idx << 32 — compacted emission, and the round's counting
+// sort by tile (sc_flush).
+struct MlWalkArgs {
+  ScatterArgs sc;         // WS, ntiles_w, log_s, hits, hitcnt, hcap, overflow
+  const uint32_t* primes; // the ML primes (ascending)
+  uint64_t* st;           // per ML prime: pos | idx << 32
+  uint32_t nml;
+  Wheel wheel;
+};
+
+__global__ void __launch_bounds__(kMlWarps * 32) k_ml_walk(const MlWalkArgs a) {
+  extern __shared__ uint4 smem_raw[];
+  MlSmem& sm = *reinterpret_cast<MlSmem*>(smem_raw);
+  uint32_t* const s_wd = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(smem_raw) + ((sizeof(MlSmem) + 15) & ~size_t{15}));
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t WS = a.WS;
-  const uint32_t B = a.ntiles_w << a.log_s;  // walk bound (the end of the last tile in the last wave)
-  const uint32_t nw = gridDim.x * kEmWarps;
+  for (uint32_t t = tid; t < kScBins; t += blockDim.x) sm.cnt[t] = 0;
+  stage_wheel(s_wd, a.wheel);
+  __syncthreads();
+  const uint32_t WS = a.sc.WS, shift = a.sc.log_s, nres = a.wheel.nres;
+  const uint32_t B = a.sc.ntiles_w << a.sc.log_s;  // walk bound (the end of the last tile in the last wave)
+  const uint32_t nw = gridDim.x * kMlWarps;
   const uint32_t nu = (a.nml + 31) / 32;
-  const uint32_t gw0 = blockIdx.x * kEmWarps + warp;
-  const uint32_t sub = gw0 % kMlSub;
-  const uint32_t st_a = smem_addr(&s_stage[warp][0]);
+  const uint32_t cnt_a = smem_addr(sm.cnt), wd_a = smem_addr(s_wd);
+  const uint32_t regw_a = smem_addr(sm.reg + warp * MlSmem::R), rankw_a = smem_addr(sm.rank + warp * MlSmem::R);
   uint32_t ltm;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+  const uint32_t gw0 = blockIdx.x * kMlWarps + warp;
   uint32_t urow = 0;
   auto unit_at = [&](uint32_t k) -> uint32_t { return k * nw + ((EG_BOUS && (k & 1)) ? nw - 1 - gw0 : gw0); };
   uint32_t u = gw0;
-  if (u >= nu) return;
   uint32_t idx = u * 32 + lane;
-  bool ok = idx < a.nml;
-  auto load = [&](uint32_t uu) -> uint2 {
+  bool ok = u < nu && idx < a.nml;
+  uint32_t p = ok ? a.primes[idx] : 0;
+  uint64_t e = ok ? a.st[idx] : 0;
+  uint32_t pos = ok ? (uint32_t)e : B, wi = (uint32_t)(e >> 32);
+  uint32_t dd = wheel_window(wd_a, nres, wi);
+  uint32_t since = 0;  // steps of this warp since its lanes loaded their delta windows
+  // the next unit's primes and states are in flight
+  uint32_t pn = 0;
+  uint64_t en = 0;
+  auto prefetch = [&](uint32_t uu) {
     const uint32_t j = uu * 32 + lane;
-    return (uu < nu && j < a.nml) ? a.ml[j] : make_uint2(0, 0);
-  };
-  uint32_t p, pos, s, c7 = 0;
-  auto decode = [&](uint2 e) {
-    if (ML7) {
-      p = e.x & 0x0fffffffu;
-      s = (e.x >> 28) & 7;
-      c7 = (e.x >> 31) | ((e.y >> 30) << 1);
-      pos = ok ? e.y & 0x3fffffffu : B;
-    } else {
-      p = e.x & 0x1fffffffu;
-      s = e.x >> 29;
-      pos = ok ? e.y : B;
+    if (uu < nu && j < a.nml) {
+      pn = a.primes[j];
+      en = a.st[j];
     }
   };
-  decode(load(u));
-  uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
-  uint2 pf = load(unit_at(1));
-  uint32_t kb = 0;  // staged records of this warp (warp-uniform)
-  auto flush = [&]() {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&a.cnt[sub], kb);
-    base = __shfl_sync(kFull, base, 0);
-    const bool over = base + kb > a.cap;
-    if (over && lane == 0) atomicExch(a.overflow, 1);
-    uint32_t* dst = a.rec + (over ? (size_t)kMlSub * a.cap : (size_t)sub * a.cap + base);
-    __syncwarp();
-    for (uint32_t i = lane; i < kb; i += 32) dst[i] = lds_u32(st_a + 4 * i);
-    __syncwarp();
-    kb = 0;
-  };
+  prefetch(unit_at(1));
+  bool live = u < nu;  // warp-uniform
   for (;;) {
-    const bool v = pos < B;
-    const uint32_t m = __ballot_sync(kFull, v);
-    if (!m) {
-      if (ok) a.ml[idx] = ML7 ? ml7_pack(p, pos - WS, s, c7) : make_uint2(p | ((s & 7) << 29), pos - WS);
-      ++urow;
-      u = unit_at(urow);
-      if (u >= nu) break;
-      idx = u * 32 + lane;
-      ok = idx < a.nml;
-      decode(pf);
-      dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
-      pf = load(unit_at(urow + 1));
-      continue;
-    }
-    if (v) {
-      sts_u32(st_a + 4 * (kb + __popc(m & ltm)), pos);
-      const uint32_t D = dd & 15u;
-      pos += D * p;
-      dd = rotr4(dd);
-      ++s;
-      if (ML7) {  // the next admissible cofactor may be divisible by 7: then take the one after
-        c7 += 2 * D;
-        c7 -= c7 >= 7 ? 7 : 0;
-        if (c7 == 0) {
-          const uint32_t D2 = dd & 15u;
-          pos += D2 * p;
-          dd = rotr4(dd);
-          ++s;
-          c7 = 2 * D2;
+    uint32_t kb = 0;  // staged records of this warp (warp-uniform)
+    while (live && kb <= (uint32_t)MlSmem::R - 32) {
+      const bool v = pos < B;
+      const uint32_t m = __ballot_sync(kFull, v);
+      if (!m) {
+        if (ok) a.st[idx] = (uint64_t)(pos - WS) | ((uint64_t)(wi >= nres ? wi - nres : wi) << 32);
+        ++urow;
+        u = unit_at(urow);
+        if (u >= nu) {
+          live = false;
+          break;
         }
-        EG_CHECK(c7 >= 1 && c7 <= 6 && pos < (1u << 30) + WS, "ML c7=%u pos=%u p=%u", c7, pos, p);
+        idx = u * 32 + lane;
+        ok = idx < a.nml;
+        p = pn;
+        pos = ok ? (uint32_t)en : B;
+        wi = (uint32_t)(en >> 32);
+        dd = wheel_window(wd_a, nres, wi);
+        since = 0;
+        prefetch(unit_at(urow + 1));
+        continue;
+      }
+      if (since == 8) {  // (warp-uniform) every lane has used at most 8 deltas of its window
+        dd = wheel_window(wd_a, nres, wi);
+        since = 0;
+      }
+      ++since;
+      const uint32_t slot = kb + __popc(m & ltm);
+      kb += __popc(m);
+      if (v) {
+        uint32_t r;
+        asm volatile(
+            "atom.shared.add.u32 %0, [%1], 1;\n\t"
+            "st.shared.u32 [%2], %3;"
+            : "=r"(r)
+            : "r"(cnt_a + ((pos >> shift) << 2)), "r"(regw_a + (slot << 2)), "r"(pos)
+            : "memory");
+        pos += (dd & 15u) * p;
+        dd >>= 4;
+        ++wi;
+        EG_CHECK(pos < 16u * WS, "ML walk pos=%u p=%u", pos, p);
+        st_rank(rankw_a + (slot << 1), r);
       }
     }
-    kb += __popc(m);
-    if (kb > (uint32_t)kEmR - 32) flush();
+    const int more = __syncthreads_or(live);
+    sc_flush<kMlWarps, kMlSteps, false, true>(sm, a.sc, kb);
+    if (!more) break;
   }
-  if (kb) flush();
 }
 
 // ---------------------------------------------------------------------------
@@ -1735,7 +1747,7 @@ __global__ void __launch_bounds__(kEmWarps * 32) k_ml_emit(const MlEmitArgs a) {
 //              the tiles' hit lists (dense: every lane holds a record).
 struct FarWalkArgs {
   const uint32_t* primes;  // the far primes (ascending)
-  uint64_t* st;            // per far prime: pos (40 bits) | s << 40 | c7 << 43
+  uint64_t* st;            // per far prime: pos (40 bits) | idx << 40
   uint32_t nfar;
   uint64_t lim;   // valid bits of this window (walk bound)
   uint64_t span;  // K * WS: the state is re-based by this after the window
@@ -1745,6 +1757,7 @@ struct FarWalkArgs {
   uint32_t* wcnt;             // [K]
   uint32_t wcap, trash_at;    // trash_at = K * wcap
   int* overflow;
+  Wheel wheel;
 };
 
 // test-only fault (ERATO_GPU_TEST_INJECT=2): a record outside its wave
@@ -1753,8 +1766,8 @@ __global__ void k_inject_wrec(uint32_t* wbuf, const uint32_t* wcnt) {
 }
 
 constexpr uint64_t kFarPosMask = (1ull << 40) - 1;
-__device__ __forceinline__ uint64_t farw_pack(uint64_t pos, uint32_t s, uint32_t c7) {
-  return (pos & kFarPosMask) | ((uint64_t)(s & 7) << 40) | ((uint64_t)c7 << 43);
+__device__ __forceinline__ uint64_t farw_pack(uint64_t pos, uint32_t idx) {
+  return (pos & kFarPosMask) | ((uint64_t)idx << 40);
 }
 
 #ifndef EG_WK_WARPS
@@ -1800,15 +1813,16 @@ __device__ __forceinline__ void scan_reserve(const uint32_t* cnt, uint32_t* off,
   }
 }
 
-template <bool FAR7>
 __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a) {
   extern __shared__ uint4 smem_raw[];
   WkSmem& sm = *reinterpret_cast<WkSmem*>(smem_raw);
+  uint32_t* const s_wd = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(smem_raw) + ((sizeof(WkSmem) + 15) & ~size_t{15}));
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr uint32_t NT = kWkWarps * 32;
   for (uint32_t t = tid; t < kScBins; t += NT) sm.cnt[t] = 0;
+  stage_wheel(s_wd, a.wheel);
   __syncthreads();
-  const uint32_t WS = a.WS, shift = a.log_s, magic = a.magic;
+  const uint32_t WS = a.WS, shift = a.log_s, magic = a.magic, nres = a.wheel.nres, wd_a = smem_addr(s_wd);
   const uint64_t lim = a.lim, span = a.span;
   const uint32_t nw = gridDim.x * kWkWarps;
   const uint32_t nu = (a.nfar + 31) / 32;
@@ -1823,14 +1837,14 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
   uint32_t idx = u * 32 + lane;
   bool ok = u < nu && idx < a.nfar;
   uint32_t p = ok ? a.primes[idx] : 0;
-  uint64_t e = ok ? a.st[idx] : ~0ull;
+  uint64_t e = ok ? a.st[idx] : 0;
   uint64_t pos;
-  uint32_t s, c7, dd;
+  uint32_t wi, dd, since = 0;  // since: steps of this warp since its lanes loaded their delta windows
   auto decode = [&]() {
     pos = ok ? (e & kFarPosMask) : lim;
-    s = (uint32_t)(e >> 40) & 7;
-    c7 = (uint32_t)(e >> 43) & 7;
-    dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+    wi = (uint32_t)(e >> 40);
+    dd = wheel_window(wd_a, nres, wi);
+    since = 0;
   };
   decode();
   // the next unit's prime and state are in flight
@@ -1851,7 +1865,7 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
       const bool v = pos < lim;
       const uint32_t m = __ballot_sync(kFull, v);
       if (!m) {
-        if (ok) a.st[idx] = farw_pack(pos - span, s, c7);
+        if (ok) a.st[idx] = farw_pack(pos - span, wi >= nres ? wi - nres : wi);
         ++urow;
         u = unit_at(urow);
         if (u >= nu) {
@@ -1866,6 +1880,11 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
         prefetch(unit_at(urow + 1));
         continue;
       }
+      if (since == 8) {  // (warp-uniform) every lane has used at most 8 deltas of its window
+        dd = wheel_window(wd_a, nres, wi);
+        since = 0;
+      }
+      ++since;
       const uint32_t slot = kb + __popc(m & ltm);
       kb += __popc(m);
       if (v) {
@@ -1880,21 +1899,9 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
             : "=r"(r)
             : "r"(cnt_a + (wv << 2)), "r"(val_a + (slot << 2)), "r"(off)
             : "memory");
-        uint32_t D = dd & 15u;
-        dd = rotr4(dd);
-        ++s;
-        if (FAR7) {  // the next admissible cofactor may be divisible by 7: then take the one after
-          c7 += 2 * D;
-          c7 -= c7 >= 7 ? 7 : 0;
-          if (c7 == 0) {
-            const uint32_t D2 = dd & 15u;
-            D += D2;
-            dd = rotr4(dd);
-            ++s;
-            c7 = 2 * D2;
-          }
-        }
-        pos += (uint64_t)D * p;
+        pos += (uint64_t)(dd & 15u) * p;
+        dd >>= 4;
+        ++wi;
         sts_u32(rb_a + (slot << 2), r | (wv << 16));
       }
     }
@@ -1985,18 +1992,17 @@ __global__ void __launch_bounds__(kWsThreads) k_wave_sort(const WaveSortArgs a) 
     }
   }
   __syncthreads();
-  for (uint32_t w = warp; w * 32 < nb; w += kWsThreads / 32) {
-    const uint32_t b = w * 32 + lane;
-    const uint32_t c = b < nb ? sm.cnt[b] : 0;
+  // scan of the tile counts: warp w takes bins 32w.. (nb <= 256 = 8 groups of
+  // the 16 warps) and sums the lower groups itself; the bin's thread reserves
+  // the run in the tile's hit list — the atomic's result is first needed
+  // after the placement, so its latency overlaps it
+  const uint32_t b = tid;  // bin of this thread (warps 0..7)
+  uint32_t c = 0, r = 0, ofs = 0;
+  if (warp * 32 < nb) {
+    c = b < nb ? sm.cnt[b] : 0;
     uint32_t low = 0;
-    for (uint32_t j = 0; j < w; ++j) low += sm.cnt[j * 32 + lane];
-    uint32_t r = 0;
-    bool over = false;
-    if (c) {
-      r = atomicAdd(&a.hitcnt[b], c);
-      over = r + c > a.hcap;
-      if (over) atomicExch(a.overflow, 1);
-    }
+    for (uint32_t j = 0; j < warp; ++j) low += sm.cnt[j * 32 + lane];
+    if (c) r = atomicAdd(&a.hitcnt[b], c);
     uint32_t x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -2005,10 +2011,9 @@ __global__ void __launch_bounds__(kWsThreads) k_wave_sort(const WaveSortArgs a) 
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) low += __shfl_xor_sync(kFull, low, o);
-    const uint32_t ofs = low + x - c;
+    ofs = low + x - c;
     if (b < nb) {
       sm.off[b] = ofs;
-      if (c) sm.gofs[b] = (over ? nb * a.hcap : b * a.hcap + r) - ofs;  // global index of sorted slot 0 of the tile
       if (b == nb - 1) sm.total = ofs + c;
     }
   }
@@ -2017,6 +2022,11 @@ __global__ void __launch_bounds__(kWsThreads) k_wave_sort(const WaveSortArgs a) 
   for (int k = 0; k < kWsPer; ++k) {
     const uint32_t t = key[k] >> shift;
     if (t < nb) sts_u32(srt_a + 4 * (lds_u32(off_a + 4 * t) + rk[k]), key[k]);
+  }
+  if (c) {
+    const bool over = r + c > a.hcap;
+    if (over) atomicExch(a.overflow, 1);
+    sm.gofs[b] = (over ? nb * a.hcap : b * a.hcap + r) - ofs;  // global index of sorted slot 0 of the tile
   }
   __syncthreads();
   const uint32_t total = sm.total;
@@ -2027,12 +2037,15 @@ __global__ void __launch_bounds__(kWsThreads) k_wave_sort(const WaveSortArgs a) 
 }
 
 static_assert(kWkWarps * WkSmem::R <= (int)kScTrash && kWsChunk <= (int)kScTrash, "trash area too small");
+static_assert(kWsThreads >= kScBins, "one thread per bin in k_wave_sort");
 
 // invariant check of a wave's far records (ERATO_GPU_CHECK_INVARIANTS): each
 // lies inside the wave's tiles
 __global__ void __launch_bounds__(256) k_check_wrecs(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_count,
-                                                     uint32_t wcap, uint32_t lim, int* bad) {
+                                                     uint32_t wcap, uint32_t lim, int* bad,
+                                                     unsigned long long* nrec) {
   const uint32_t n = min(*in_count, wcap);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(nrec, (unsigned long long)n);
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
     if (in[j] >= lim) atomicExch(bad, 1);
 }
@@ -2191,7 +2204,12 @@ struct SetupArgs {
   int inject;  // test-only fault injection on the first far prime: 1 drop its entry, 2 corrupt its q
   int far7;    // far entries in the mod-210 format (far7_pack)
   int ml7;     // ML states in the mod-210 format (ml7_pack)
-  uint64_t* fst;  // windowed far path: per far prime state (farw_pack) instead of bucket entries
+  // wheel mode (default path): ML states pos | idx << 32, far states farw_pack(pos, idx); idx = rank of the
+  // first hit's cofactor among the residues coprime to wM (wrank[c mod wM])
+  uint64_t* fst;
+  uint64_t* mlst;
+  const uint16_t* wrank;
+  uint32_t wM, wmask;  // wmask: bit 0/1/2 = the wheel also excludes cofactors divisible by 7/11/13
 };
 
 constexpr int kSetupThreads = 1024;
@@ -2211,7 +2229,26 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     // keeps the first hit within 3.5p of the interval start in overlap runs
     uint64_t cof = 0;
     uint64_t pos = first_hit(p, a.x0, 2, s, &cof);
-    if (i < a.i_ml_end) {
+    if (a.wrank) {
+      // along the mod-30 wheel to the first cofactor coprime to the whole wheel modulus
+      uint32_t cm = (uint32_t)(cof % a.wM);  // cofactor mod the wheel modulus
+      while (((a.wmask & 1) && cm % 7 == 0) || ((a.wmask & 2) && cm % 11 == 0) || ((a.wmask & 4) && cm % 13 == 0)) {
+        const uint32_t D = wheel_D(s);
+        pos += (uint64_t)D * p;
+        cm += 2 * D;
+        cm -= cm >= a.wM ? a.wM : 0;
+        s = (s + 1) & 7;
+      }
+      const uint32_t wi = a.wrank[cm];
+      EG_CHECK(wi != 0xffffu, "cofactor not on the wheel p=%u", p);
+      if (i < a.i_ml_end) {
+        EG_CHECK(pos < (1ull << 32), "first ML hit beyond 32 bits p=%u", p);
+        a.mlst[i - a.i0] = pos | ((uint64_t)wi << 32);
+      } else {
+        if (a.inject == 1 && i == a.i_ml_end) pos = kFarPosMask;  // test-only: the prime never hits
+        a.fst[i - a.i_ml_end] = farw_pack(pos, wi);
+      }
+    } else if (i < a.i_ml_end) {
       if (a.ml7) {  // skip a first hit whose cofactor 7 divides (the next one cannot)
         uint32_t c7 = (uint32_t)(cof % 7);
         if (c7 == 0) {
@@ -2235,15 +2272,11 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
           s = (s + 1) & 7;
         }
       }
-      if (a.fst) {  // first hit relative to the run start (= start of window 0)
-        if (a.inject == 1 && i == a.i_ml_end) pos = kFarPosMask;  // test-only: the prime never hits
-        a.fst[i - a.i_ml_end] = farw_pack(pos, s, a.far7 ? c7 : 1);
-      }
       // d = pos / WS: fp64 estimate (pos < 2^40, off by at most one), exact fix
       uint64_t d = __double2ull_rz(__dmul_rz(__ull2double_rz(pos), a.inv_ws));
       if (d * a.WS > pos) --d;
       if ((d + 1) * a.WS <= pos) ++d;
-      if (!a.fst && d < a.nwaves) {
+      if (d < a.nwaves) {
         app = true;
         slotb = (uint32_t)d % a.ring;
         const uint32_t q = (uint32_t)(pos - d * a.WS);
@@ -2301,6 +2334,20 @@ __device__ __forceinline__ uint64_t coprime30_upto(uint64_t n) {  // #{1 <= c <=
 __device__ __forceinline__ uint64_t coprime210_upto(uint64_t n) {  // #{1 <= c <= n : gcd(c, 210) = 1}
   return coprime30_upto(n) - coprime30_upto(n / 7);  // c coprime to 30 and divisible by 7: c = 7c', c' coprime to 30
 }
+// #{1 <= c <= n : gcd(c, 30) = 1 and none of the primes selected by mask (bit 0/1/2 = 7/11/13) divides c}
+__device__ __forceinline__ uint64_t coprime_wheel_upto(uint64_t n, uint32_t mask) {
+  const uint32_t q[3] = {7, 11, 13};
+  uint64_t tot = 0;
+  for (uint32_t sub = 0; sub < 8; ++sub) {  // inclusion-exclusion over the subsets of the selected primes
+    if (sub & ~mask) continue;
+    uint64_t d = 1;
+    for (int k = 0; k < 3; ++k)
+      if (sub >> k & 1) d *= q[k];
+    const uint64_t t = coprime30_upto(n / d);
+    tot = (__popc(sub) & 1) ? tot - t : tot + t;
+  }
+  return tot;
+}
 __device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {
   // fp64 estimate (off by at most one), exact fix on the remainder in
   // wrap-around u64 arithmetic (q*p may pass 2^64 when x is near it)
@@ -2313,7 +2360,7 @@ __device__ __forceinline__ uint64_t div_floor(uint64_t x, uint32_t p) {
 __global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __restrict__ primes, uint64_t i0,
                                                           uint64_t i1, uint64_t x_lo, uint64_t x_hi,
                                                           unsigned long long* __restrict__ out, uint64_t i7_lo,
-                                                          uint64_t i7_hi) {
+                                                          uint64_t i7_hi, uint32_t wmask) {
   const uint64_t i = i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long cnt = 0;
   if (i < i1) {
@@ -2322,7 +2369,7 @@ __global__ void __launch_bounds__(256) k_expected_records(const uint32_t* __rest
     if (c_lo < 2) c_lo = 2;
     const uint64_t c_hi = div_floor(x_hi, p);
     if (c_hi >= c_lo)
-      cnt = i >= i7_lo && i < i7_hi ? coprime210_upto(c_hi) - coprime210_upto(c_lo - 1)  // primes skipping 7 | c
+      cnt = i >= i7_lo && i < i7_hi ? coprime_wheel_upto(c_hi, wmask) - coprime_wheel_upto(c_lo - 1, wmask)
                                     : coprime30_upto(c_hi) - coprime30_upto(c_lo - 1);
   }
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);

@@ -215,6 +215,10 @@ class RunStats:
     ml_primes: int = 0
     far_primes: int = 0
     skip7: int = 0
+    wheel: int = 0
+    far_records: int = 0
+    walk_s: float = 0.0
+    far_windows: int = 0
 
     @classmethod
     def _from(cls, s: _lib.Stats) -> "RunStats":
@@ -226,7 +230,8 @@ class RunStats:
                    tiles=s.tiles, log_tile=s.log_tile, waves=s.waves, kernel_launches=s.kernel_launches,
                    retries=s.retries, gen_s=s.gen_s, bin_s=s.bin_s, large_records=s.large_records,
                    medium_primes=s.medium_primes, ml_primes=s.ml_primes, far_primes=s.far_primes,
-                   skip7=s.skip7)
+                   skip7=s.skip7, wheel=s.wheel, far_records=s.far_records, walk_s=s.walk_s,
+                   far_windows=s.far_windows)
 
 
 @dataclass

@@ -429,7 +429,7 @@ def test_random_large_geometries_invariants_and_mr(gpu_ctx):
 
 @pytest.mark.parametrize("l,f,n", [(22, (1 << 37) - 4096, 300), (21, (1 << 26) - 2048, 300), (20, 1 << 21, 60)])
 def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
-    """Large primes may skip their multiples whose cofactor 7 divides (mod-210
+    """(Legacy structures, ERATO_GPU_LARGE=legacy.)  Large primes may skip their multiples whose cofactor 7 divides (mod-210
     far entries / ML states; those numbers are marked by the pattern of 7).
     Every combination — both off (pure mod-30), default, both forced on —
     gives the same table, and the large-prime invariants (records consumed ==
@@ -438,8 +438,9 @@ def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
     p = E.validate_params(l, f, n)
     results = []
     for env in ({"ERATO_GPU_FAR7": "0", "ERATO_GPU_ML7": "0"}, {}, {"ERATO_GPU_ML7": "1"}):
-        old = {k: os.environ.get(k) for k in ("ERATO_GPU_FAR7", "ERATO_GPU_ML7")}
+        old = {k: os.environ.get(k) for k in ("ERATO_GPU_FAR7", "ERATO_GPU_ML7", "ERATO_GPU_LARGE")}
         os.environ.update(env)
+        os.environ["ERATO_GPU_LARGE"] = "legacy"  # (the mod-30/210 states of the round-1/2 structures)
         try:
             st = gpu_ctx.count(p, check_invariants=True)
             t, _ = gpu_ctx.table(p)
@@ -458,17 +459,21 @@ def test_mod210_record_skipping_matches_mod30(gpu_ctx, l, f, n):
 @pytest.mark.parametrize("l,f,n", [(22, (1 << 37) - 4096, 700), (21, (1 << 26) - 2048, 300), (20, 1 << 21, 60),
                                    (22, (1 << 37) - 4096, 37)])
 def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
-    """The default large-prime pipeline — unsorted ML records (k_ml_emit), the
-    windowed far walk (k_far_walk), one partition by tile per wave
-    (k_wave_sort) — gives the same table as every older path it replaced: the
-    sorting ML scatter, the per-wave far bucket ring, a far class starting
-    below the wave span, several windows per run."""
+    """The default large-prime pipeline — table-driven mod-30030 wheel walks
+    (k_ml_walk per wave, k_far_walk per window of waves) and one partition by
+    tile per wave (k_wave_sort) — gives the same table as every other wheel
+    modulus, as the legacy structures it replaced (mod-30/210 states, the
+    sorting ML scatter, the per-wave far bucket ring), with a far class
+    starting below the wave span and with one or many windows per run; the
+    large-prime invariants hold on each, and a finer wheel makes fewer
+    records."""
     import paper_1111_3297_b200 as E
     p = E.validate_params(l, f, n)
-    keys = ("ERATO_GPU_FAR", "ERATO_GPU_ML", "ERATO_GPU_FAR_DIV", "ERATO_GPU_FAR_WINDOW")
-    results = []
-    for env in ({}, {"ERATO_GPU_FAR": "ring"}, {"ERATO_GPU_ML": "emit"},
-                {"ERATO_GPU_FAR": "ring", "ERATO_GPU_ML": "emit"},
+    keys = ("ERATO_GPU_LARGE", "ERATO_GPU_WHEEL", "ERATO_GPU_FAR_DIV", "ERATO_GPU_FAR_WINDOW", "ERATO_GPU_FAR7",
+            "ERATO_GPU_ML7")
+    results, records = [], {}
+    for env in ({}, {"ERATO_GPU_WHEEL": "30"}, {"ERATO_GPU_WHEEL": "210"}, {"ERATO_GPU_WHEEL": "2310"},
+                {"ERATO_GPU_LARGE": "legacy"}, {"ERATO_GPU_LARGE": "legacy", "ERATO_GPU_FAR7": "0", "ERATO_GPU_ML7": "0"},
                 {"ERATO_GPU_FAR_DIV": "4", "ERATO_GPU_FAR_WINDOW": "2"}, {"ERATO_GPU_FAR_WINDOW": "1"}):
         old = {k: os.environ.get(k) for k in keys}
         os.environ.update(env)
@@ -482,7 +487,13 @@ def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
                 else:
                     os.environ[k] = v
         results.append((st.prime_count, sha(t)))
+        if "ERATO_GPU_LARGE" not in env and "ERATO_GPU_FAR_DIV" not in env and "ERATO_GPU_FAR_WINDOW" not in env:
+            records[int(env.get("ERATO_GPU_WHEEL", "30030"))] = st.large_records
+            assert st.wheel == int(env.get("ERATO_GPU_WHEEL", "30030"))
+        assert st.far_records <= st.large_records
     assert len(set(results)) == 1, results
+    if l >= 21:
+        assert records[30030] < records[2310] < records[210] < records[30]
 
 
 @pytest.mark.parametrize("limit", [4096, 92681, 1049087, 16777471, 1073741839])
