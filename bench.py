@@ -439,6 +439,7 @@ def run_ours(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": head["ms"],
+        "step_ms": [round(t * 1e3, 3) for t in head["times"]],  # this rank's timed steps, one by one
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,

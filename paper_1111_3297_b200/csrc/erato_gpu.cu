@@ -8,10 +8,12 @@
 //        prime list (popcount + scan compaction)
 //     3. one host sync: prime count, class boundaries, largest prime
 //     4. large primes: first hits (fp64 quotient estimate + exact u64
-//        remainder) -> ML array + far wave buckets
+//        remainder), advanced to the first cofactor on the mod-30030 wheel
+//        -> ML states / far states (next hit + wheel index)
 //   waves (the reference's per-segment loop, driver.cpp:93-117)
-//     for each wave of W tiles: k_scatter_ml + k_scatter_far (large primes
-//     -> per-tile hit records, far entries re-bucketed) then k_tile
+//     per window of K waves: k_far_walk (far primes -> per-wave record buckets)
+//     for each wave of W tiles: k_ml_walk (ML primes -> per-tile hit records),
+//     k_wave_sort (the wave's far records -> per-tile hit records), then k_tile
 //     (patterns, medium primes, hits, popcount, 128-bit write-out)
 //   count: device u64 (NullSink: only it leaves the device).
 #include <cuda_runtime.h>
@@ -112,6 +114,7 @@ struct erato_gpu_ctx {
   DevBuf mlst;                                // wheel mode: ML states (pos | idx << 32)
   DevBuf wdelta, wrank;                       // wheel tables of the large primes (cached per modulus)
   uint32_t wheel_M = 0, wheel_nres = 0;
+  size_t mem_free0 = 0;                       // free device memory when the context was created
   double hcap_scale = 1.0, bcap_scale = 1.0;
   uint64_t max_base_pairs = uint64_t{1} << 27;  // base.hpp:87
   cudaEvent_t ev[4] = {};
@@ -259,6 +262,10 @@ int create_impl(erato_gpu_ctx* c) {
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   c->nsm = prop.multiProcessorCount;
+  {
+    size_t mem_total = 0;
+    CUDA_TRY(cudaMemGetInfo(&c->mem_free0, &mem_total));
+  }
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming));
@@ -737,9 +744,8 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         const uint64_t nwin = (P.nwaves + kwin_max - 1) / kwin_max;
         kwin = (uint32_t)((P.nwaves + nwin - 1) / nwin);
         // (the window's record buckets: at most 6 GiB and a quarter of the device memory that is free now)
-        size_t mem_free = 0, mem_total = 0;
-        CUDA_TRY(cudaMemGetInfo(&mem_free, &mem_total));
-        const uint64_t wbudget = std::min<uint64_t>(6ull << 30, std::max<uint64_t>(mem_free / 4 + c->wbuf.cap, 64ull << 20));
+        // (free memory as of the context's creation: cudaMemGetInfo costs milliseconds, not per run)
+        const uint64_t wbudget = std::min<uint64_t>(6ull << 30, std::max<uint64_t>(c->mem_free0 / 4, 64ull << 20));
         while (kwin > 1 && ((uint64_t)kwin * wcap + eg::kScTrash >= (1ull << 32) || (uint64_t)kwin * wcap * 4 > wbudget))
           kwin = (kwin + 1) / 2;
         wmagic = (uint32_t)((1ull << 32) / P.W) + 1;  // umulhi(t, wmagic) = t / W for t * W < 2^32

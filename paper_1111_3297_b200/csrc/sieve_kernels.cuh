@@ -15,12 +15,16 @@
 //                          residues (k_med_records), mod-30 wheel over the
 //                          cofactor (wheel.cpp:10-69 idea: 8 of 15 odd
 //                          cofactors)
-//   ML      S < p <= W*S   walked once per wave (k_scatter_ml) into per-tile
-//                          hit records
-//   far     p > W*S        (p,q) entries in the bucket of the wave of their
-//                          next hit (k_scatter_far): the paper's circle /
-//                          bucket idea (large_kernel.hpp, Lemma 2)
-//                          rebuilt for a machine that sieves 148 tiles at once
+//   ML      S < p <= W*S/4 walked once per wave (k_ml_walk) into per-tile
+//                          hit records; a table-driven mod-30030 wheel over the
+//                          cofactor (the reference's wheel three primes further)
+//   far     p > W*S/4      walked once per window of K waves (k_far_walk) into
+//                          the record bucket of the wave of each hit — the
+//                          paper's bucket of the segment of the next hit
+//                          (large_kernel.hpp, Lemma 2) filled K waves
+//                          ahead — and split by tile per wave (k_wave_sort)
+//   (k_scatter_ml / k_scatter_far / k_gen / k_bin: the round-1/2 structures,
+//   ERATO_GPU_LARGE=legacy and the fallback for waves of more than 256 tiles)
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -1943,7 +1947,13 @@ struct WaveSortArgs {
   uint32_t hcap;
   int* overflow;
 };
-constexpr int kWsThreads = 512, kWsPer = 8, kWsChunk = kWsThreads * kWsPer;
+#ifndef EG_WS_THREADS
+#define EG_WS_THREADS 512
+#endif
+#ifndef EG_WS_PER
+#define EG_WS_PER 8
+#endif
+constexpr int kWsThreads = EG_WS_THREADS, kWsPer = EG_WS_PER, kWsChunk = kWsThreads * kWsPer;
 struct WsSmem {
   uint32_t srt[kWsChunk];
   uint32_t cnt[kScBins], off[kScBins], gofs[kScBins];
