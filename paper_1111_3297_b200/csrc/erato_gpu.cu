@@ -104,6 +104,9 @@ struct erato_gpu_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t xstream = nullptr;               // D2H copies of finished waves (sieve_to_host)
   cudaEvent_t xev = nullptr, xjoin = nullptr;   // wave done / copies done
+  // k_wave_sort runs beside k_ml_walk on a side stream (both only append to the hit lists)
+  cudaStream_t sstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
   // cached per context
   DevBuf sp, spm, ptab;  // small primes < 2^16, their base-sieve records, pattern tables
   std::vector<uint32_t> h_sp;
@@ -270,6 +273,10 @@ int create_impl(erato_gpu_ctx* c) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&c->xjoin, cudaEventDisableTiming));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->sstream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_sorted, cudaEventDisableTiming));
+
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   for (auto& e : c->ev_copy) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CUDA_TRY(cudaMallocHost(&c->hflags, kOutSlots * sizeof(uint64_t)));
@@ -335,6 +342,7 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->xstream) cudaStreamSynchronize(c->xstream);
+  if (c->sstream) cudaStreamSynchronize(c->sstream);
   for (DevBuf* b : {&c->sp, &c->spm, &c->ptab, &c->base_bits, &c->primes, &c->med, &c->ml, &c->buckets,
                     &c->bcount, &c->hits, &c->hitcnt, &c->blk_cnt, &c->blk_off, &c->scal, &c->table,
                     &c->outbuf, &c->recs, &c->rcount, &c->frecs, &c->fslot, &c->fcount, &c->slices, &c->fst,
@@ -350,6 +358,10 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   if (c->xev) cudaEventDestroy(c->xev);
   if (c->xjoin) cudaEventDestroy(c->xjoin);
   if (c->xstream) cudaStreamDestroy(c->xstream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_sorted) cudaEventDestroy(c->ev_sorted);
+  if (c->sstream) cudaStreamDestroy(c->sstream);
+
   if (c->stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
   delete c;
@@ -927,6 +939,11 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
     uint32_t ml_blocks = c->nsm, far_blocks = c->nsm, walk_blocks = c->nsm;
     const bool winfar = win && nfar > 0;
     const bool wml = win && nml > 0;  // wheel-mode ML walk (k_ml_walk)
+    // the wave's far-record partition beside the ML walk (not with per-launch timing events)
+    const char* cs_env = std::getenv("ERATO_GPU_SORT_STREAM");
+    const bool conc_sort = !timing && !(cs_env && std::strcmp(cs_env, "0") == 0);
+    int ml_ctas = 0;  // ML-walk CTAs per SM (0: as many as fit)
+    if (const char* e = std::getenv("ERATO_GPU_ML_CTAS")) ml_ctas = std::atoi(e);
     const size_t wsm_ml = ((sizeof(eg::MlSmem) + 15) & ~size_t{15}) + c->wheel_nres / 2 + 4;
     const size_t wsm_far = ((sizeof(eg::WkSmem) + 15) & ~size_t{15}) + c->wheel_nres / 2 + 4;
     eg::Wheel wheel{c->wdelta.as<uint32_t>(), c->wheel_nres};
@@ -941,6 +958,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_ml_walk, eg::kMlWarps * 32, wsm_ml));
       const uint64_t units = (nml + 31) / 32;
+      if (ml_ctas > 0) occ = std::min(occ, ml_ctas);
       mlw_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
                                                 std::max<uint64_t>(1, (units + eg::kMlWarps - 1) / eg::kMlWarps));
       mwa.primes = c->primes.as<uint32_t>() + iS;
@@ -1024,7 +1042,29 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         uint32_t* const hitcnt_w = c->hitcnt.as<uint32_t>() + (uint64_t)wi * P.W;
         ta.hits = hits_w;
         ta.hitcnt = hitcnt_w;
+        cudaStream_t sst = st;  // stream of the wave's far-record partition
         if (split) {
+          if (winfar && (uint32_t)(w % kwin) == 0) {  // a new window: walk the far primes through its waves
+            const uint64_t tiles_left = P.ntiles - tile0;
+            fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
+            fwa.lim = std::min<uint64_t>((uint64_t)kwin * P.W, tiles_left) << P.log_s;
+            CUDA_TRY(cudaMemsetAsync(c->wcnt.p, 0, (uint64_t)eg::kScBins * 4, sst));
+            if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 1], st));
+            eg::k_far_walk<<<walk_blocks, eg::kWkWarps * 32, wsm_far, sst>>>(fwa);
+            if (timing) {
+              CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 2], st));
+              walk_ev.push_back(nev - 2 * walk_ev.size() - 1);
+            }
+            launches += 1;
+            if (w == 0 && sa_inject == 2) eg::k_inject_wrec<<<1, 1, 0, sst>>>(fwa.wbuf, fwa.wcnt);  // tests only
+            if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));  // (the wave's ML interval starts here)
+          }
+          // k_wave_sort runs beside k_ml_walk on the side stream: both only append to the hit lists
+          if (conc_sort && winfar && wml) {
+            sst = c->sstream;
+            CUDA_TRY(cudaEventRecord(c->ev_fork, st));
+            CUDA_TRY(cudaStreamWaitEvent(sst, c->ev_fork, 0));
+          }
           if (wml) {
             mwa.sc = sca;
             mwa.sc.ntiles_w = ntw;
@@ -1046,24 +1086,10 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           uint32_t nseg = 0, max_cap = 0;  // record segments k_wave_sort partitions by tile
           if (winfar) {
             const uint32_t wl = (uint32_t)(w % kwin);
-            if (wl == 0) {  // a new window: walk the far primes through its waves
-              const uint64_t tiles_left = P.ntiles - tile0;
-              fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
-              fwa.lim = std::min<uint64_t>((uint64_t)kwin * P.W, tiles_left) << P.log_s;
-              CUDA_TRY(cudaMemsetAsync(c->wcnt.p, 0, (uint64_t)eg::kScBins * 4, st));
-              if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 1], st));
-              eg::k_far_walk<<<walk_blocks, eg::kWkWarps * 32, wsm_far, st>>>(fwa);
-              if (timing) {
-                CUDA_TRY(cudaEventRecord(c->phase_ev[nev - 2 * walk_ev.size() - 2], st));
-                walk_ev.push_back(nev - 2 * walk_ev.size() - 1);
-              }
-              launches += 1;
-              if (w == 0 && sa_inject == 2) eg::k_inject_wrec<<<1, 1, 0, st>>>(fwa.wbuf, fwa.wcnt);  // tests only
-            }
             const uint32_t* in = c->wbuf.as<uint32_t>() + (uint64_t)wl * wcap;
             const uint32_t* in_count = c->wcnt.as<uint32_t>() + wl;
             if (flags & ERATO_GPU_CHECK_INVARIANTS) {
-              eg::k_check_wrecs<<<(unsigned)c->nsm, 256, 0, st>>>(in, in_count, wcap, ntw << P.log_s,
+              eg::k_check_wrecs<<<(unsigned)c->nsm, 256, 0, sst>>>(in, in_count, wcap, ntw << P.log_s,
                                                                   reinterpret_cast<int*>(d_scal + 21),
                                                                   reinterpret_cast<unsigned long long*>(d_scal + 23));
               ++launches;
@@ -1090,8 +1116,12 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
             wsa.hits = hits_w;
             wsa.hitcnt = hitcnt_w;
             const uint32_t chunks = (max_cap + eg::kWsChunk - 1) / eg::kWsChunk;
-            eg::k_wave_sort<<<dim3(chunks, nseg), eg::kWsThreads, 0, st>>>(wsa);
+            eg::k_wave_sort<<<dim3(chunks, nseg), eg::kWsThreads, 0, sst>>>(wsa);
             launches += 1;
+          }
+          if (sst != st) {  // join before the tiles
+            CUDA_TRY(cudaEventRecord(c->ev_sorted, sst));
+            CUDA_TRY(cudaStreamWaitEvent(st, c->ev_sorted, 0));
           }
         } else {
           // k_gen walks the ML primes wave by wave (any ML bound works)
@@ -1222,7 +1252,6 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         }
         stats->gen_s = tg * 1e-3;
         stats->masks_s = (double)res[6] * 1e-9;
-        stats->bin_s = tb * 1e-3;
         double tw = 0;
         for (const size_t e0 : walk_ev) {
           float ms = 0;
@@ -1230,6 +1259,9 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
           tw += ms;
         }
         stats->walk_s = tw * 1e-3;
+        tb += tw;  // (the walks run before their window's first wave interval)
+        tl += tw;
+        stats->bin_s = tb * 1e-3;
         stats->small_s = ts * 1e-3;
         stats->large_s = tl * 1e-3;
       }
