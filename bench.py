@@ -308,6 +308,8 @@ def roofline(m, world: int):
                             "k_far_walk": round(ph.walk_s * 1e3, 3),
                             "k_wave_sort": round((ph.bin_s - ph.walk_s) * 1e3, 3), "init": round(ph.init_s * 1e3, 3),
                             "masks_phase_cta0": round(ph.masks_s * 1e3, 3)},
+        "kernel_split_note": "from one extra pass with CUDA events around every launch; there k_wave_sort runs after "
+                             "k_ml_walk, in the timed steps beside it on a side stream (the sum exceeds ms_per_step)",
         "large_prime_wheel": ph.wheel,
     }
     # ---- per-kernel: algorithmic bytes per launch / average launch time ----

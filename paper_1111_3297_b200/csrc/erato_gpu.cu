@@ -829,6 +829,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         sa.mlst = c->mlst.as<uint64_t>();
         sa.wrank = c->wrank.as<uint16_t>();
         sa.wM = wheel_M;
+        sa.wR32 = (uint32_t)((1ull << 32) % wheel_M);
         sa.wmask = wmask;
       }
       const uint64_t nl = nprimes - iS;

@@ -2219,7 +2219,7 @@ struct SetupArgs {
   uint64_t* fst;
   uint64_t* mlst;
   const uint16_t* wrank;
-  uint32_t wM, wmask;  // wmask: bit 0/1/2 = the wheel also excludes cofactors divisible by 7/11/13
+  uint32_t wM, wR32, wmask;  // wR32 = 2^32 mod wM; wmask: bit 0/1/2 = the wheel also excludes cofactors divisible by 7/11/13
 };
 
 constexpr int kSetupThreads = 1024;
@@ -2241,7 +2241,8 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     uint64_t pos = first_hit(p, a.x0, 2, s, &cof);
     if (a.wrank) {
       // along the mod-30 wheel to the first cofactor coprime to the whole wheel modulus
-      uint32_t cm = (uint32_t)(cof % a.wM);  // cofactor mod the wheel modulus
+      // cofactor mod the wheel modulus without a 64-bit division: 2^32 = wR32 (mod wM)
+      uint32_t cm = (((uint32_t)(cof >> 32) % a.wM) * a.wR32 + (uint32_t)cof % a.wM) % a.wM;
       while (((a.wmask & 1) && cm % 7 == 0) || ((a.wmask & 2) && cm % 11 == 0) || ((a.wmask & 4) && cm % 13 == 0)) {
         const uint32_t D = wheel_D(s);
         pos += (uint64_t)D * p;

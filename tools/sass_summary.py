@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 SO = sys.argv[1] if len(sys.argv) > 1 else "paper_1111_3297_b200/liberato_gpu.so"
-HOT = ("k_tile", "k_scatter_ml", "k_scatter_far", "k_setup_large")
+HOT = ("k_tile", "k_ml_walk", "k_far_walk", "k_wave_sort", "k_scatter_ml", "k_scatter_far", "k_setup_large")
 KEY = ("ATOMS", "RED", "ATOMG", "LDGSTS", "LDG", "STG", "LDS", "STS", "BAR", "SHFL", "VOTE", "MATCH", "CALL", "MUFU",
        "DMUL", "I2F", "F2I")
 
@@ -39,7 +39,7 @@ def main():
         if "k_setup_large" not in f:  # the wave kernels; setup runs once per run (fp64 reciprocal slow path)
             calls += c["CALL"]
         print(f[:58].ljust(58), str(sum(c.values())).rjust(5), " ".join(str(c[k]).rjust(6) for k in KEY))
-    print(f"# CALL instructions in the wave kernels (k_tile, k_scatter_ml*, k_scatter_far): {calls} (must be 0)")
+    print(f"# CALL instructions in the wave kernels (k_tile, k_ml_walk, k_far_walk, k_wave_sort, legacy k_scatter_*): {calls} (must be 0)")
     return 1 if calls else 0
 
 
