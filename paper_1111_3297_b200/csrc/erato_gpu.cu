@@ -960,7 +960,9 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_ml_walk, eg::kMlWarps * 32, wsm_ml));
       const uint64_t units = (nml + 31) / 32;
       if (ml_ctas > 0) occ = std::min(occ, ml_ctas);
-      mlw_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+      int over = 1;  // CTAs per resident slot (more, shorter CTAs: the hardware scheduler evens out the tail)
+      if (const char* e = std::getenv("ERATO_GPU_ML_OVER")) over = std::max(1, std::atoi(e));
+      mlw_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1) * over,
                                                 std::max<uint64_t>(1, (units + eg::kMlWarps - 1) / eg::kMlWarps));
       mwa.primes = c->primes.as<uint32_t>() + iS;
       mwa.st = c->mlst.as<uint64_t>();
@@ -971,7 +973,9 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, eg::k_far_walk, eg::kWkWarps * 32, wsm_far));
       const uint64_t units = (nfar + 31) / 32;
-      walk_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1),
+      int wover = 16;  // (cfg5: 1 / 2 / 4 / 8 / 16 CTAs per resident slot = 8.87 / 8.74 / 8.60 / 8.44 / 8.35 ms of far walk)
+      if (const char* e = std::getenv("ERATO_GPU_WALK_OVER")) wover = std::max(1, std::atoi(e));
+      walk_blocks = (uint32_t)std::min<uint64_t>((uint64_t)c->nsm * (uint32_t)std::max(occ, 1) * wover,
                                                  std::max<uint64_t>(1, (units + eg::kWkWarps - 1) / eg::kWkWarps));
       fwa.primes = c->primes.as<uint32_t>() + iWS;
       fwa.st = c->fst.as<uint64_t>();

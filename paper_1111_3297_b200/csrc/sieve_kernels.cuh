@@ -2299,6 +2299,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
       }
     }
   }
+  if (a.wrank) return;  // (wheel mode: no bucket appends; uniform over the grid)
   // CTA-level aggregation of the bucket appends: the first hits of all far
   // primes fall into the first few waves, so per-warp atomics on those few
   // counters would serialise
