@@ -267,6 +267,12 @@ def measure(R: Rank, cfg: int, steps: int, warmup: int):
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         torch.cuda.synchronize()
+        # short configs (cfg1-3: a millisecond per step): keep the same load running, untimed, until the
+        # clock sampler (one nvidia-smi line per 50 ms) has seen it
+        t_load = time.perf_counter()
+        while sum(times) < 0.5 and time.perf_counter() - t_load < 0.6:
+            step()
+        torch.cuda.synchronize()
         R.barrier()
     t_max = R.allreduce(sum(times), "max")
     total_count = int(count.item())
