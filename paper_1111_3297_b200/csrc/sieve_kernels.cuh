@@ -209,7 +209,7 @@ __global__ void k_build_patterns(uint32_t* __restrict__ ptab) {
 // (first_offset, src/wheel.cpp:43-47) and wheel_align (src/wheel.cpp:60-69)
 // per (prime, tile) without 64-bit division.
 constexpr uint32_t kMaxChunkTiles = 1u << 20;
-constexpr uint32_t kMedPad = 2048;  // records past the end the tile kernel may prefetch
+constexpr uint32_t kMedPad = 4096;  // records past the end the tile kernel may prefetch (up to three items of 1024)
 
 __global__ void k_med_records(const uint32_t* __restrict__ primes, uint32_t n, uint64_t x0, uint32_t log_s,
                               uint4* __restrict__ out) {
@@ -245,6 +245,15 @@ struct TileArgs {
   unsigned long long* phase_ns;  // nullable: CTA 0 adds its pattern-phase time (masks_s)
 };
 
+#ifndef EG_ITEM_UNROLL2
+#define EG_ITEM_UNROLL2 1  // lane-per-prime items two per trip (cfg5 k_tile 21.0 -> 20.1 ms; cfg2-4 unchanged)
+#endif
+#ifndef EG_EVERY_NUM
+#define EG_EVERY_NUM 1  // hit-chunk cadence: one chunk per (items / (chunks + 1)) * NUM / DEN medium items
+#endif
+#ifndef EG_EVERY_DEN
+#define EG_EVERY_DEN 1
+#endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 2048;  // medium primes below S/64 (pi(16384) = 1900 at S = 2^20)
 constexpr uint32_t kHitChunk = 256;        // hit records per warp chunk (1 KB of shared staging per warp)
@@ -470,9 +479,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
     };
     issue();
     // one chunk per `every` medium items of this warp
-    const uint32_t my_items = (nitems + (a.nmed - a.nmed_warp + 31) / 32 + kTileWarps - 1) / kTileWarps;
+#ifndef EG_HITS_GROUPW
+#define EG_HITS_GROUPW 0  // weight (in quarters) of a group-marked item in the hit-chunk cadence (a lane-per-prime item = 4): the
+                          // records are consumed between the ALU-heavy lane-per-prime items only (cfg5 0 / 2 / 4 / 8: 45.58 / 45.81 / 45.82 / 45.91 ms)
+#endif
+    const uint32_t my_items = (nitems * EG_HITS_GROUPW / 4 + (a.nmed - a.nmed_warp + 31) / 32 + kTileWarps - 1) / kTileWarps;
     const uint32_t my_chunks = (nch + kTileWarps - 1) / kTileWarps;
-    const uint32_t every = my_chunks ? max(1u, my_items / (my_chunks + 1)) : 0xffffffffu;
+    const uint32_t every = my_chunks ? max(1u, my_items * EG_EVERY_NUM / ((my_chunks + 1) * EG_EVERY_DEN)) : 0xffffffffu;
     uint32_t since = 0;
     // static round-robin (no barrier follows: the lane-per-prime phase
     // absorbs the imbalance)
@@ -505,17 +518,80 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
         mark_a(tile_a, q + 3 * step);
       }
       for (; q < S; q += step) mark_a(tile_a, q);
-      if (HITS && ++since >= every) {
+      if (HITS && EG_HITS_GROUPW && (since += EG_HITS_GROUPW) >= 4 * every) {
         since = 0;
         consume();
       }
     }
+    since = 0;
     // 2b. lane-per-prime (S/64 <= p): whole wheel periods unrolled for
     // p <= S/8, a plain wheel walk for the few-mark primes above
     const uint32_t nlane = a.nmed - a.nmed_warp;
     const uint32_t nitem = (nlane + 31) / 32;
     // the record array is padded (kMedPad): next item's record in flight
     const uint4* rp = a.med + a.nmed_warp + warp * 32 + lane;
+#if EG_ITEM_UNROLL2
+    auto process = [&](const uint4 cur, const uint32_t item) {
+      const bool valid = item * 32 + lane < nlane;
+      if (valid) {
+        uint32_t p, s;
+        uint32_t q = med_first<P2>(cur, t, tf, x_t, combo_a, p, s);
+#ifndef EG_TWO_HIT
+#define EG_TWO_HIT 1
+#endif
+        if (EG_TWO_HIT && (p << 1) > S) {  // p > S/2: hits are > S/2 apart, at most two in the tile
+          if (q < S) {
+            mark_a(tile_a, q);
+            q += wheel_D(s) * p;
+            if (q < S) mark_a(tile_a, q);
+          }
+        } else if ((p << 3) > S) {
+          uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);  // low nibble = wheel_D(s)
+          while (q < S) {
+            mark_a(tile_a, q);
+            q += (dd & 15u) * p;
+            dd = __funnelshift_r(dd, dd, 4);
+          }
+        } else {
+          const uint32_t cp = s_cum[s];
+          const uint32_t o1 = p * nib(cp, 1), o2 = p * nib(cp, 2), o3 = p * nib(cp, 3), o4 = p * nib(cp, 4),
+                         o5 = p * nib(cp, 5), o6 = p * nib(cp, 6), o7 = p * nib(cp, 7);
+          const uint32_t per = 15u * p;
+          for (; q + o7 < S; q += per) {
+            mark_a(tile_a, q);
+            mark_a(tile_a, q + o1);
+            mark_a(tile_a, q + o2);
+            mark_a(tile_a, q + o3);
+            mark_a(tile_a, q + o4);
+            mark_a(tile_a, q + o5);
+            mark_a(tile_a, q + o6);
+            mark_a(tile_a, q + o7);
+          }
+          // last partial period: a short wheel walk from class s
+          uint32_t dd = __funnelshift_r(0x13212123u, 0x13212123u, 4 * s);
+          while (q < S) {
+            mark_a(tile_a, q);
+            q += (dd & 15u) * p;
+            dd = __funnelshift_r(dd, dd, 4);
+          }
+        }
+      }
+      if (HITS && (since += 4) >= 4 * every) {
+        since = 0;
+        consume();
+      }
+    };
+    // two items per trip, their records in two register sets (no copies), the next two in flight
+    uint4 rA = *rp, rB = rp[kTileWarps * 32];
+    for (uint32_t item = warp; item < nitem; item += 2 * kTileWarps) {
+      rp += 2 * kTileWarps * 32;
+      const uint4 cA = rA, cB = rB;
+      rA = rp[0];
+      rB = rp[kTileWarps * 32];
+      process(cA, item);
+      if (item + kTileWarps < nitem) process(cB, item + kTileWarps);
+    }
+#else
     uint4 rec = *rp;
     for (uint32_t item = warp; item < nitem; item += kTileWarps) {
       const uint4 cur = rec;
@@ -565,11 +641,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
           }
         }
       }
-      if (HITS && ++since >= every) {
+      if (HITS && (since += 4) >= 4 * every) {
         since = 0;
         consume();
       }
     }
+#endif
     while (HITS && pend) consume();  // this warp's remaining hit chunks
   }
   __syncthreads();
