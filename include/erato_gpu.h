@@ -119,6 +119,13 @@ uint32_t erato_gpu_first_offset(uint32_t p, unsigned l, uint64_t f);
  * c mod 30 = 1,7,11,13,17,19,23,29).  With x = u this is Lemma 1 +
  * wheel_align (src/wheel.cpp:43-69) in one step. */
 int erato_gpu_first_hit(uint32_t p, uint64_t x, uint64_t cmin, uint64_t* offset, unsigned* wheel_class);
+/* The large primes' wheel (the reference's mod-30 wheel, src/wheel.cpp:10-34,
+ * taken to modulus M = 30, 210, 2310 or 30030): writes delta[i] = half the gap
+ * from the i-th odd residue coprime to M to the next one (wrapping) for
+ * i < min(count, cap) and returns the residue count (8, 48, 480, 5760), 0 for
+ * another M.  A large prime p marks c*p only for cofactors c on this wheel;
+ * the index offset from one hit to the next is delta[i] * p. */
+size_t erato_gpu_wheel_deltas(uint32_t M, uint8_t* delta, size_t cap);
 /* table_filename (src/driver.cpp:17-20); returns bytes needed incl. NUL. */
 size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, size_t cap);
 /* errc_name (src/params.cpp:7-21) for codes 1..10, plus the GPU codes. */

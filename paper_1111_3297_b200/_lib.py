@@ -23,7 +23,7 @@ EXPORTS = (
     "erato_gpu_count", "erato_gpu_write_table", "erato_gpu_shard", "erato_gpu_extract_primes",
     "erato_gpu_first_hit", "erato_gpu_set_max_base_pairs", "erato_gpu_run_to_sink",
     "erato_gpu_multi_create", "erato_gpu_multi_destroy", "erato_gpu_multi_uses_nccl",
-    "erato_gpu_multi_count", "erato_gpu_multi_write_table", "erato_gpu_base_primes",
+    "erato_gpu_multi_count", "erato_gpu_multi_write_table", "erato_gpu_base_primes", "erato_gpu_wheel_deltas",
 )
 
 COUNT_OVERFLOW = (1 << 64) - 1  # ERATO_GPU_COUNT_OVERFLOW
@@ -97,6 +97,8 @@ def load(path: str = SO_PATH):
     L.erato_gpu_write_table.argtypes = [C.c_void_p, C.c_char_p, C.c_uint, C.c_uint64, C.c_uint64,
                                         C.c_uint64, C.c_uint64, C.c_uint, C.c_char_p, C.c_size_t,
                                         C.POINTER(Stats)]
+    L.erato_gpu_wheel_deltas.restype = C.c_size_t
+    L.erato_gpu_wheel_deltas.argtypes = [C.c_uint32, u8p, C.c_size_t]
     L.erato_gpu_shard.restype = None
     L.erato_gpu_shard.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, u64p, u64p]
     L.erato_gpu_extract_primes.restype = C.c_int

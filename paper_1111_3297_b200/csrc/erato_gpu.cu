@@ -91,6 +91,9 @@ uint64_t pi_upper(uint64_t x) {
   return (uint64_t)(1.25506 * (double)x / std::log((double)x)) + 16;
 }
 
+bool wheel_residues(uint32_t M, std::vector<uint32_t>& res, std::vector<uint16_t>* rank);
+uint32_t wheel_delta(const std::vector<uint32_t>& res, uint32_t M, size_t i);
+
 constexpr uint32_t kBaseLogTile = 20;  // tile size for the sieve of [1, sqrt(v)]
 constexpr uint32_t kGenBlocksPerSm = 2;
 constexpr uint64_t kFewLarge = 2048;  // at most this many primes > S are sieved as medium primes
@@ -233,6 +236,13 @@ size_t erato_gpu_table_filename(unsigned l, uint64_t f, uint64_t n, char* out, s
                         std::to_string(n) + ".bits";
   if (out && cap) std::snprintf(out, cap, "%s", s.c_str());
   return s.size() + 1;
+}
+
+size_t erato_gpu_wheel_deltas(uint32_t M, uint8_t* delta, size_t cap) {
+  std::vector<uint32_t> res;
+  if (!wheel_residues(M, res, nullptr)) return 0;
+  for (size_t i = 0; i < res.size() && i < cap && delta; ++i) delta[i] = (uint8_t)wheel_delta(res, M, i);
+  return res.size();
 }
 
 void erato_gpu_shard(uint64_t f, uint64_t n, int rank, int world, uint64_t* f_out, uint64_t* n_out) {
@@ -466,21 +476,30 @@ int base_primes(erato_gpu_ctx* c, cudaStream_t st, uint64_t vroot, uint32_t& lau
 // Wheel tables of the large primes for modulus M (30, 210, 2310 or 30030):
 // delta[i] = half the gap from the i-th residue coprime to M to the next one
 // (wrapping), rank[r] = index of residue r (0xffff if not coprime).  Cached.
+// residues coprime to M (odd, ascending) and their ranks; false for an unsupported modulus
+bool wheel_residues(uint32_t M, std::vector<uint32_t>& res, std::vector<uint16_t>* rank) {
+  if (M != 30 && M != 210 && M != 2310 && M != 30030) return false;
+  res.clear();
+  if (rank) rank->assign(M, 0xffff);
+  for (uint32_t r = 1; r < M; r += 2)
+    if (r % 3 && r % 5 && (M % 7 || r % 7) && (M % 11 || r % 11) && (M % 13 || r % 13)) {
+      if (rank) (*rank)[r] = (uint16_t)res.size();
+      res.push_back(r);
+    }
+  return true;
+}
+uint32_t wheel_delta(const std::vector<uint32_t>& res, uint32_t M, size_t i) {  // half gap to the next residue (<= 11)
+  return ((i + 1 < res.size() ? res[i + 1] : res[0] + M) - res[i]) / 2;
+}
+
 int ensure_wheel(erato_gpu_ctx* c, cudaStream_t st, uint32_t M) {
   if (c->wheel_M == M) return 0;
   std::vector<uint32_t> res;
-  std::vector<uint16_t> rank(M, 0xffff);
-  for (uint32_t r = 1; r < M; r += 2)
-    if (r % 3 && r % 5 && (M % 7 || r % 7) && (M % 11 || r % 11) && (M % 13 || r % 13)) {
-      rank[r] = (uint16_t)res.size();
-      res.push_back(r);
-    }
-  if (res.size() > eg::kWheelMaxRes || res.size() % 8) return fail(ERATO_GPU_E_INVALID_ARG, "wheel size");
+  std::vector<uint16_t> rank;
+  if (!wheel_residues(M, res, &rank) || res.size() > eg::kWheelMaxRes || res.size() % 8)
+    return fail(ERATO_GPU_E_INVALID_ARG, "wheel modulus");
   std::vector<uint32_t> delta(res.size() / 8 + 1, 0);  // 8 nibbles per word + the wrap-around word
-  for (size_t i = 0; i < res.size(); ++i) {
-    const uint32_t nxt = i + 1 < res.size() ? res[i + 1] : res[0] + M;
-    delta[i / 8] |= ((nxt - res[i]) / 2) << (4 * (i % 8));  // half gaps <= 11
-  }
+  for (size_t i = 0; i < res.size(); ++i) delta[i / 8] |= wheel_delta(res, M, i) << (4 * (i % 8));
   delta.back() = delta[0];
   CUDA_TRY(c->wdelta.ensure(eg::kWheelMaxBytes));
   CUDA_TRY(c->wrank.ensure((size_t)30030 * 2));

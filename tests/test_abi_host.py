@@ -160,3 +160,28 @@ def test_header_flags_and_gpu_errc_match_python_mirror(lib):
                       ("ERATO_GPU_E_INVARIANT", E.errc.invariant)]:
         assert codes[cname] == int(py) + 1
         assert lib.erato_gpu_errc_name(codes[cname]).decode() == E.errc_name(py)
+
+
+def test_wheel_deltas_walk_the_coprime_cofactors(lib):
+    """erato_gpu_wheel_deltas: the large primes' wheel tables.  For every
+    supported modulus the deltas walk exactly the odd residues coprime to M
+    (the reference's wheel, src/wheel.cpp:10-34, is the M = 30 case with
+    deltas {3,2,1,2,1,2,3,1}), sum to M/2 per turn and fit a nibble."""
+    import ctypes as C
+    from math import gcd
+    assert lib.erato_gpu_wheel_deltas(77, None, 0) == 0
+    for M, nres in ((30, 8), (210, 48), (2310, 480), (30030, 5760)):
+        buf = (C.c_uint8 * nres)()
+        assert lib.erato_gpu_wheel_deltas(M, buf, nres) == nres
+        d = list(buf)
+        assert sum(d) == M // 2 and max(d) <= 11 and min(d) >= 1
+        r, seen = 1, []
+        for x in d:
+            seen.append(r)
+            r += 2 * x
+        assert r == 1 + M  # one full turn
+        assert seen == [c for c in range(1, M, 2) if gcd(c, M) == 1]
+    buf = (C.c_uint8 * 8)()
+    lib.erato_gpu_wheel_deltas(30, buf, 8)
+    assert list(buf) == [3, 2, 1, 2, 1, 2, 3, 1]  # wheel.cpp:27-30
+
