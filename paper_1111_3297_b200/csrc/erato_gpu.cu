@@ -110,6 +110,8 @@ struct erato_gpu_ctx {
   // k_wave_sort runs beside k_ml_walk on a side stream (both only append to the hit lists)
   cudaStream_t sstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_sorted = nullptr;
+  // early partition (ERATO_GPU_EARLY_SORT): wave w+1's far records are partitioned while wave w runs
+  cudaEvent_t ev_walk = nullptr, ev_tile[2] = {}, ev_sort[2] = {};
   // cached per context
   DevBuf sp, spm, ptab;  // small primes < 2^16, their base-sieve records, pattern tables
   std::vector<uint32_t> h_sp;
@@ -286,6 +288,11 @@ int create_impl(erato_gpu_ctx* c) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->sstream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&c->ev_sorted, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_walk, cudaEventDisableTiming));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_tile[k], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_sort[k], cudaEventDisableTiming));
+  }
 
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   for (auto& e : c->ev_copy) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -370,6 +377,11 @@ void erato_gpu_destroy(erato_gpu_ctx* c) {
   if (c->xstream) cudaStreamDestroy(c->xstream);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_sorted) cudaEventDestroy(c->ev_sorted);
+  if (c->ev_walk) cudaEventDestroy(c->ev_walk);
+  for (int k = 0; k < 2; ++k) {
+    if (c->ev_tile[k]) cudaEventDestroy(c->ev_tile[k]);
+    if (c->ev_sort[k]) cudaEventDestroy(c->ev_sort[k]);
+  }
   if (c->sstream) cudaStreamDestroy(c->sstream);
 
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -706,6 +718,13 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
   if (const char* e = std::getenv("ERATO_GPU_FAR_WINDOW")) kwin_max = (uint32_t)std::max(1, std::atoi(e));
   kwin_max = std::min<uint32_t>(kwin_max, eg::kScBins);
 
+  // Early partition (default; ERATO_GPU_EARLY_SORT=0: the wave's own partition beside its ML walk): wave
+  // w+1's far records are split by tile on the side stream while wave w's ML walk and tiles run, into a
+  // second set of hit lists (cfg5 45.6 -> 44.9 ms; with a 16 KB smaller k_tile and 256-thread partition
+  // CTAs that fit beside a tile CTA: 48.3 ms)
+  const char* es_env = std::getenv("ERATO_GPU_EARLY_SORT");
+  const bool early_req = win && !(flags & (ERATO_GPU_PHASE_TIMING | ERATO_GPU_CHECK_INVARIANTS)) &&
+                         !(es_env && std::strcmp(es_env, "0") == 0);
   uint32_t launches = 0;
   for (int attempt = 0;; ++attempt) {
     const uint64_t vroot = isqrt_u64(P.v);
@@ -764,9 +783,10 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       CUDA_TRY(c->ml.ensure(std::max<uint64_t>(nml, 1) * 8));
       if (win) CUDA_TRY(c->mlst.ensure(std::max<uint64_t>(nml, 1) * 8));
       // the lists of the MW waves of an ML window, + trash of the split scatter
-      CUDA_TRY(c->hits.ensure(((uint64_t)P.MW * P.W * hcap + eg::kScTrash) * 4));
-      CUDA_TRY(c->hitcnt.ensure((uint64_t)P.MW * P.W * 4));
-      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)P.MW * P.W * 4, st));
+      const uint32_t nlists = early_req ? 2 : P.MW;
+      CUDA_TRY(c->hits.ensure(((uint64_t)nlists * P.W * hcap + eg::kScTrash) * 4));
+      CUDA_TRY(c->hitcnt.ensure((uint64_t)nlists * P.W * 4));
+      CUDA_TRY(cudaMemsetAsync(c->hitcnt.p, 0, (uint64_t)nlists * P.W * 4, st));
       if (nfar && win) {
         const double sr_far = std::max(0.0, std::log(lnP / std::log((double)p_ml))) + 0.01;
         const double ew = (double)P.WS * wdens * sr_far;  // records per wave
@@ -776,7 +796,9 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         kwin = (uint32_t)((P.nwaves + nwin - 1) / nwin);
         // (the window's record buckets: at most 6 GiB and a quarter of the device memory that is free now)
         // (free memory as of the context's creation: cudaMemGetInfo costs milliseconds, not per run)
-        const uint64_t wbudget = std::min<uint64_t>(6ull << 30, std::max<uint64_t>(c->mem_free0 / 4, 64ull << 20));
+        uint64_t wmax = 6ull << 30;
+        if (const char* e = std::getenv("ERATO_GPU_FAR_BUDGET_GB")) wmax = (uint64_t)std::max(1, std::atoi(e)) << 30;
+        const uint64_t wbudget = std::min<uint64_t>(wmax, std::max<uint64_t>(c->mem_free0 / 4, 64ull << 20));
         while (kwin > 1 && ((uint64_t)kwin * wcap + eg::kScTrash >= (1ull << 32) || (uint64_t)kwin * wcap * 4 > wbudget))
           kwin = (kwin + 1) / 2;
         wmagic = (uint32_t)((1ull << 32) / P.W) + 1;  // umulhi(t, wmagic) = t / W for t * W < 2^32
@@ -1061,13 +1083,56 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         ga.far_in_count = c->bcount.as<uint32_t>() + slot;
         if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
         // this wave's hit lists inside the ML window's lists
-        const uint32_t wi = (uint32_t)(w % P.MW);
+        const bool early = early_req && winfar && wml;
+        const uint32_t wi = early ? (uint32_t)(w & 1) : (uint32_t)(w % P.MW);
         uint32_t* const hits_w = c->hits.as<uint32_t>() + (uint64_t)wi * P.W * hcap;
         uint32_t* const hitcnt_w = c->hitcnt.as<uint32_t>() + (uint64_t)wi * P.W;
         ta.hits = hits_w;
         ta.hitcnt = hitcnt_w;
         cudaStream_t sst = st;  // stream of the wave's far-record partition
-        if (split) {
+        if (split && early) {
+          // wave x's far records -> the hit lists x & 1, on the side stream, as soon as those lists' last
+          // tiles (wave x - 2) are done and the window's walk has filled the bucket
+          auto issue_sort = [&](uint64_t x) -> int {
+            const uint32_t bx = (uint32_t)(x & 1), xl = (uint32_t)(x % kwin);
+            cudaStream_t ss = c->sstream;
+            CUDA_TRY(cudaStreamWaitEvent(ss, x >= 2 ? c->ev_tile[bx] : c->ev_fork, 0));
+            if (xl == 0) CUDA_TRY(cudaStreamWaitEvent(ss, c->ev_walk, 0));
+            wsa.in[0] = c->wbuf.as<uint32_t>() + (uint64_t)xl * wcap;
+            wsa.in_count[0] = c->wcnt.as<uint32_t>() + xl;
+            wsa.cap[0] = wcap;
+            wsa.nb = (uint32_t)std::min<uint64_t>(P.W, P.ntiles - x * P.W);
+            wsa.hits = c->hits.as<uint32_t>() + (uint64_t)bx * P.W * hcap;
+            wsa.hitcnt = c->hitcnt.as<uint32_t>() + (uint64_t)bx * P.W;
+            eg::k_wave_sort<<<dim3((wcap + eg::kWsChunk - 1) / eg::kWsChunk, 1), eg::kWsThreads, 0, ss>>>(wsa);
+            CUDA_TRY(cudaEventRecord(c->ev_sort[bx], ss));
+            launches += 1;
+            return 0;
+          };
+          if (w == 0) CUDA_TRY(cudaEventRecord(c->ev_fork, st));
+          if ((uint32_t)(w % kwin) == 0) {  // a new window: walk the far primes through its waves
+            const uint64_t tiles_left = P.ntiles - tile0;
+            fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
+            fwa.lim = std::min<uint64_t>((uint64_t)kwin * P.W, tiles_left) << P.log_s;
+            CUDA_TRY(cudaMemsetAsync(c->wcnt.p, 0, (uint64_t)eg::kScBins * 4, st));
+            eg::k_far_walk<<<walk_blocks, eg::kWkWarps * 32, wsm_far, st>>>(fwa);
+            launches += 1;
+            CUDA_TRY(cudaEventRecord(c->ev_walk, st));
+            rc = issue_sort(w);
+            if (rc) return rc;
+          }
+          mwa.sc = sca;
+          mwa.sc.ntiles_w = ntw;
+          mwa.sc.hits = hits_w;
+          mwa.sc.hitcnt = hitcnt_w;
+          eg::k_ml_walk<<<mlw_blocks, eg::kMlWarps * 32, wsm_ml, st>>>(mwa);
+          launches += 1;
+          if (w + 1 < P.nwaves && (uint32_t)((w + 1) % kwin) != 0) {
+            rc = issue_sort(w + 1);
+            if (rc) return rc;
+          }
+          CUDA_TRY(cudaStreamWaitEvent(st, c->ev_sort[wi], 0));
+        } else if (split) {
           if (winfar && (uint32_t)(w % kwin) == 0) {  // a new window: walk the far primes through its waves
             const uint64_t tiles_left = P.ntiles - tile0;
             fwa.nbins = (uint32_t)std::min<uint64_t>(kwin, P.nwaves - w);
@@ -1187,6 +1252,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       }
       if (timing) CUDA_TRY(cudaEventRecord(c->phase_ev[evi], st));
       launch_tiles(st, ta, ntw, P.overlap);
+      if (have_large && early_req && winfar && nml) CUDA_TRY(cudaEventRecord(c->ev_tile[w & 1], st));
       if (out) {  // output pipeline: this wave's bytes go to the host now
         const uint64_t b0 = (tile0 << P.log_s) / 8, b1 = std::min<uint64_t>((tile0 + ntw) << P.log_s, P.T) / 8;
         CUDA_TRY(cudaEventRecord(c->xev, st));
@@ -1204,6 +1270,10 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
         evi += 2;
       }
       ++launches;
+    }
+    if (early_req) {  // join the side stream (a partition may be pending after an early exit of the loop)
+      CUDA_TRY(cudaEventRecord(c->ev_sorted, c->sstream));
+      CUDA_TRY(cudaStreamWaitEvent(st, c->ev_sorted, 0));
     }
     if (out) {  // join the copies
       CUDA_TRY(cudaEventRecord(c->xjoin, c->xstream));

@@ -256,7 +256,11 @@ struct TileArgs {
 #endif
 constexpr int kTileThreads = 1024;
 constexpr uint32_t kMaxWarpPrimes = 2048;  // medium primes below S/64 (pi(16384) = 1900 at S = 2^20)
-constexpr uint32_t kHitChunk = 256;        // hit records per warp chunk (1 KB of shared staging per warp)
+#ifndef EG_HIT_CHUNK
+#define EG_HIT_CHUNK 256
+#endif
+constexpr uint32_t kHitChunk = EG_HIT_CHUNK;  // hit records per warp chunk (1 KB of shared staging per warp): 256 or 128
+static_assert(kHitChunk == 256 || kHitChunk == 128, "one or two uint4 per lane");
 constexpr int kTileWarps = kTileThreads / 32;
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       if (HITS && ch < nch) {
         const uint32_t* src = hl + ch * kHitChunk + 4 * lane;
         cp_async16(hst_a, src);
-        cp_async16(hst_a + 512, src + 128);
+        if (kHitChunk == 256) cp_async16(hst_a + 512, src + 128);
         cp_async_commit();
         pend = true;
       }
@@ -454,13 +458,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile(const TileArgs a) {
       if constexpr (HITS) {
         if (!pend) return;
         cp_async_wait_all();
-        const uint4 v0 = s_hits[warp * (kHitChunk / 4) + lane], v1 = s_hits[warp * (kHitChunk / 4) + 32 + lane];
-        const uint32_t i0 = ch * kHitChunk + 4 * lane, i1 = i0 + 128;
+        const uint4 v0 = s_hits[warp * (kHitChunk / 4) + lane];
+        const uint4 v1 = kHitChunk == 256 ? s_hits[warp * (kHitChunk / 4) + 32 + lane] : make_uint4(0, 0, 0, 0);
+        const uint32_t i0 = ch * kHitChunk + 4 * lane, i1 = kHitChunk == 256 ? i0 + 128 : hcnt;
         EG_CHECK(i0 >= hcnt || (v0.x < S && (i0 + 3 >= hcnt || v0.w < S)), "hit record beyond the tile %u %u", v0.x, v0.w);
         EG_CHECK(i1 >= hcnt || (v1.x < S && (i1 + 3 >= hcnt || v1.w < S)), "hit record beyond the tile %u %u", v1.x, v1.w);
-        if (i1 + 3 < hcnt) {
+        if (kHitChunk == 256 ? i1 + 3 < hcnt : i0 + 3 < hcnt) {
           mark_a(tile_a, v0.x); mark_a(tile_a, v0.y); mark_a(tile_a, v0.z); mark_a(tile_a, v0.w);
-          mark_a(tile_a, v1.x); mark_a(tile_a, v1.y); mark_a(tile_a, v1.z); mark_a(tile_a, v1.w);
+          if (kHitChunk == 256) {
+            mark_a(tile_a, v1.x); mark_a(tile_a, v1.y); mark_a(tile_a, v1.z); mark_a(tile_a, v1.w);
+          }
         } else {
           if (i0 < hcnt) mark_a(tile_a, v0.x);
           if (i0 + 1 < hcnt) mark_a(tile_a, v0.y);

@@ -464,17 +464,19 @@ def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
     tile per wave (k_wave_sort) — gives the same table as every other wheel
     modulus, as the legacy structures it replaced (mod-30/210 states, the
     sorting ML scatter, the per-wave far bucket ring), with a far class
-    starting below the wave span and with one or many windows per run; the
-    large-prime invariants hold on each, and a finer wheel makes fewer
-    records."""
+    starting elsewhere, with one or many windows per run, and with the
+    partition of a wave's far records early (default), beside or after its ML
+    walk; the large-prime invariants hold on each, and a finer wheel makes
+    fewer records."""
     import paper_1111_3297_b200 as E
     p = E.validate_params(l, f, n)
     keys = ("ERATO_GPU_LARGE", "ERATO_GPU_WHEEL", "ERATO_GPU_FAR_DIV", "ERATO_GPU_FAR_WINDOW", "ERATO_GPU_FAR7",
-            "ERATO_GPU_ML7")
+            "ERATO_GPU_ML7", "ERATO_GPU_EARLY_SORT", "ERATO_GPU_SORT_STREAM")
     results, records = [], {}
     for env in ({}, {"ERATO_GPU_WHEEL": "30"}, {"ERATO_GPU_WHEEL": "210"}, {"ERATO_GPU_WHEEL": "2310"},
                 {"ERATO_GPU_LARGE": "legacy"}, {"ERATO_GPU_LARGE": "legacy", "ERATO_GPU_FAR7": "0", "ERATO_GPU_ML7": "0"},
-                {"ERATO_GPU_FAR_DIV": "4", "ERATO_GPU_FAR_WINDOW": "2"}, {"ERATO_GPU_FAR_WINDOW": "1"}):
+                {"ERATO_GPU_FAR_DIV": "8", "ERATO_GPU_FAR_WINDOW": "2"}, {"ERATO_GPU_FAR_WINDOW": "1"},
+                {"ERATO_GPU_EARLY_SORT": "0"}, {"ERATO_GPU_EARLY_SORT": "0", "ERATO_GPU_SORT_STREAM": "0"}):
         old = {k: os.environ.get(k) for k in keys}
         os.environ.update(env)
         try:
@@ -487,7 +489,7 @@ def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
                 else:
                     os.environ[k] = v
         results.append((st.prime_count, sha(t)))
-        if "ERATO_GPU_LARGE" not in env and "ERATO_GPU_FAR_DIV" not in env and "ERATO_GPU_FAR_WINDOW" not in env:
+        if not env or "ERATO_GPU_WHEEL" in env:
             records[int(env.get("ERATO_GPU_WHEEL", "30030"))] = st.large_records
             assert st.wheel == int(env.get("ERATO_GPU_WHEEL", "30030"))
         assert st.far_records <= st.large_records
