@@ -498,6 +498,23 @@ def test_large_prime_path_variants_identical(gpu_ctx, l, f, n):
         assert records[30030] < records[2310] < records[210] < records[30]
 
 
+@pytest.mark.parametrize("l", [10, 13, 14])
+def test_few_tiles_large_primes_vs_reference(gpu_ctx, reference, l):
+    """Runs of 1..33 segments (a handful of small tiles per wave, one wave, a
+    far window of one wave) whose base primes are far above the tile: the ML
+    class may be empty (every large prime is a far prime), the far bucket tiny,
+    the last wave ragged.  Tables and counts against the reference run_sieve,
+    with the large-prime invariants on."""
+    import paper_1111_3297_b200 as E
+    for n in (1, 2, 3, 5, 8, 17, 33):
+        for f in ((1 << 30) + 12345, 987654321):
+            p = E.validate_params(l, f, n)
+            t, st = gpu_ctx.table(p)
+            rt, rc, _ = reference.run_sieve(l, f, n, table=True)
+            assert st.prime_count == rc and np.array_equal(t, rt), (l, f, n)
+            assert gpu_ctx.count(p, check_invariants=True).prime_count == rc
+
+
 @pytest.mark.parametrize("limit", [4096, 92681, 1049087, 16777471, 1073741839])
 def test_base_prime_list_equals_reference_simple_sieve(reference, limit):
     """The device base-prime list (odd primes <= isqrt(v) of cfg1..cfg5),
