@@ -513,10 +513,18 @@ int ensure_wheel(erato_gpu_ctx* c, cudaStream_t st, uint32_t M) {
   std::vector<uint32_t> delta(res.size() / 8 + 1, 0);  // 8 nibbles per word + the wrap-around word
   for (size_t i = 0; i < res.size(); ++i) delta[i / 8] |= wheel_delta(res, M, i) << (4 * (i % 8));
   delta.back() = delta[0];
+  // for a cofactor residue c coprime to 30: the first wheel residue >= c (index | half the gap << 16)
+  std::vector<uint32_t> next(M, 0xffffffffu);
+  for (uint32_t cm = 1; cm < M; cm += 2) {
+    if (cm % 3 == 0 || cm % 5 == 0) continue;
+    uint32_t c = cm;
+    while (rank[c % M] == 0xffff) c += 2;
+    next[cm] = rank[c % M] | (((c - cm) / 2) << 16);
+  }
   CUDA_TRY(c->wdelta.ensure(eg::kWheelMaxBytes));
-  CUDA_TRY(c->wrank.ensure((size_t)30030 * 2));
+  CUDA_TRY(c->wrank.ensure((size_t)30030 * 4));
   CUDA_TRY(cudaMemcpyAsync(c->wdelta.p, delta.data(), delta.size() * 4, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(c->wrank.p, rank.data(), rank.size() * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(c->wrank.p, next.data(), next.size() * 4, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // (the host vectors go out of scope)
   c->wheel_M = M;
   c->wheel_nres = (uint32_t)res.size();
@@ -868,7 +876,7 @@ int run_impl(erato_gpu_ctx* c, unsigned l, uint64_t f, uint64_t n, unsigned flag
       if (win) {
         sa.fst = c->fst.as<uint64_t>();
         sa.mlst = c->mlst.as<uint64_t>();
-        sa.wrank = c->wrank.as<uint16_t>();
+        sa.wnext = c->wrank.as<uint32_t>();
         sa.wM = wheel_M;
         sa.wR32 = (uint32_t)((1ull << 32) % wheel_M);
         sa.wmask = wmask;

@@ -2299,10 +2299,10 @@ struct SetupArgs {
   int far7;    // far entries in the mod-210 format (far7_pack)
   int ml7;     // ML states in the mod-210 format (ml7_pack)
   // wheel mode (default path): ML states pos | idx << 32, far states farw_pack(pos, idx); idx = rank of the
-  // first hit's cofactor among the residues coprime to wM (wrank[c mod wM])
+  // first hit's cofactor among the residues coprime to wM
   uint64_t* fst;
   uint64_t* mlst;
-  const uint16_t* wrank;
+  const uint32_t* wnext;  // [wM], for c mod wM coprime to 30: index of the first wheel residue >= c | half the gap to it << 16
   uint32_t wM, wR32, wmask;  // wR32 = 2^32 mod wM; wmask: bit 0/1/2 = the wheel also excludes cofactors divisible by 7/11/13
 };
 
@@ -2310,8 +2310,10 @@ constexpr int kSetupThreads = 1024;
 
 __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a) {
   __shared__ uint32_t s_cnt[kScBins], s_base[kScBins];
-  for (uint32_t b = threadIdx.x; b < kScBins; b += blockDim.x) s_cnt[b] = 0;
-  __syncthreads();
+  if (!a.wnext) {  // (legacy bucket appends only; uniform over the grid)
+    for (uint32_t b = threadIdx.x; b < kScBins; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+  }
   const uint64_t i = a.i0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool app = false;
   uint32_t slotb = 0;
@@ -2323,19 +2325,15 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
     // keeps the first hit within 3.5p of the interval start in overlap runs
     uint64_t cof = 0;
     uint64_t pos = first_hit(p, a.x0, 2, s, &cof);
-    if (a.wrank) {
-      // along the mod-30 wheel to the first cofactor coprime to the whole wheel modulus
-      // cofactor mod the wheel modulus without a 64-bit division: 2^32 = wR32 (mod wM)
-      uint32_t cm = (((uint32_t)(cof >> 32) % a.wM) * a.wR32 + (uint32_t)cof % a.wM) % a.wM;
-      while (((a.wmask & 1) && cm % 7 == 0) || ((a.wmask & 2) && cm % 11 == 0) || ((a.wmask & 4) && cm % 13 == 0)) {
-        const uint32_t D = wheel_D(s);
-        pos += (uint64_t)D * p;
-        cm += 2 * D;
-        cm -= cm >= a.wM ? a.wM : 0;
-        s = (s + 1) & 7;
-      }
-      const uint32_t wi = a.wrank[cm];
-      EG_CHECK(wi != 0xffffu, "cofactor not on the wheel p=%u", p);
+    if (a.wnext) {
+      // from the first cofactor coprime to 30 to the first one on the whole wheel: one table entry per
+      // cofactor residue (its index on the wheel, and how far ahead it is); the cofactor mod the wheel
+      // modulus without a 64-bit division: 2^32 = wR32 (mod wM)
+      const uint32_t cm = (((uint32_t)(cof >> 32) % a.wM) * a.wR32 + (uint32_t)cof % a.wM) % a.wM;
+      const uint32_t nx = a.wnext[cm];
+      EG_CHECK(nx != 0xffffffffu, "cofactor not coprime to 30 p=%u", p);
+      pos += (uint64_t)(nx >> 16) * p;
+      const uint32_t wi = nx & 0xffffu;
       if (i < a.i_ml_end) {
         EG_CHECK(pos < (1ull << 32), "first ML hit beyond 32 bits p=%u", p);
         a.mlst[i - a.i0] = pos | ((uint64_t)wi << 32);
@@ -2383,7 +2381,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_setup_large(const SetupArgs a
       }
     }
   }
-  if (a.wrank) return;  // (wheel mode: no bucket appends; uniform over the grid)
+  if (a.wnext) return;  // (wheel mode: no bucket appends; uniform over the grid)
   // CTA-level aggregation of the bucket appends: the first hits of all far
   // primes fall into the first few waves, so per-warp atomics on those few
   // counters would serialise
