@@ -1878,26 +1878,46 @@ struct WkSmem {
 };
 
 // Exclusive scan of cnt[0..nb) into off by warp 0 while the other warps
-// reserve c slots per non-empty bin in gcnt[b]: gofs[b] = global index of the
-// bin's first reserved slot (the caller subtracts off[b] after the barrier).
+// reserve c slots per non-empty bin in gcnt[b].  The atomics' results stay in
+// registers (rsv) until reserve_finish, after the placement, so their latency
+// overlaps the scan and the placement; a thread holds at most two bins.
+struct Resv {
+  uint32_t c0, c1, r0, r1;  // counts and reserved starts of bins tid - 32 and tid - 32 + (NT - 32)
+};
 template <int NW>
-__device__ __forceinline__ void scan_reserve(const uint32_t* cnt, uint32_t* off, uint32_t* gofs, uint32_t* total,
-                                             uint32_t nb, uint32_t* gcnt, uint32_t cap, uint32_t trash_at,
-                                             int* overflow) {
-  const uint32_t tid = threadIdx.x;
+__device__ __forceinline__ void scan_reserve(const uint32_t* cnt, uint32_t* off, uint32_t* total, uint32_t nb,
+                                             uint32_t* gcnt, Resv& rsv) {
+  static_assert(kScBins <= 2 * (NW * 32 - 32), "two reservations per thread");
+  const uint32_t tid = threadIdx.x, b0 = tid - 32, b1 = b0 + (NW * 32 - 32);
+  rsv.c0 = rsv.c1 = rsv.r0 = rsv.r1 = 0;
   if (tid < 32) {
     const uint32_t tot = warp_excl_scan(cnt, off, nb);
     if (tid == 0) *total = tot;
   } else {
-    for (uint32_t b = tid - 32; b < nb; b += NW * 32 - 32) {
-      const uint32_t c = cnt[b];
-      if (c) {
-        const uint32_t r = atomicAdd(&gcnt[b], c);
-        const bool over = r + c > cap;
-        if (over) atomicExch(overflow, 1);
-        gofs[b] = over ? trash_at : b * cap + r;
-      }
+    if (b0 < nb) {
+      rsv.c0 = cnt[b0];
+      if (rsv.c0) rsv.r0 = atomicAdd(&gcnt[b0], rsv.c0);
     }
+    if (b1 < nb) {
+      rsv.c1 = cnt[b1];
+      if (rsv.c1) rsv.r1 = atomicAdd(&gcnt[b1], rsv.c1);
+    }
+  }
+}
+// gofs[b] = global index of sorted slot 0 of bin b
+template <int NW>
+__device__ __forceinline__ void reserve_finish(const Resv& rsv, const uint32_t* off, uint32_t* gofs, uint32_t cap,
+                                               uint32_t trash_at, int* overflow) {
+  const uint32_t b0 = threadIdx.x - 32, b1 = b0 + (NW * 32 - 32);
+  if (rsv.c0) {
+    const bool over = rsv.r0 + rsv.c0 > cap;
+    if (over) atomicExch(overflow, 1);
+    gofs[b0] = (over ? trash_at : b0 * cap + rsv.r0) - off[b0];
+  }
+  if (rsv.c1) {
+    const bool over = rsv.r1 + rsv.c1 > cap;
+    if (over) atomicExch(overflow, 1);
+    gofs[b1] = (over ? trash_at : b1 * cap + rsv.r1) - off[b1];
   }
 }
 
@@ -1995,7 +2015,8 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
     }
     const int more = __syncthreads_or(live);
     // ---- round: sort this round's records by wave, coalesced runs out ----
-    scan_reserve<kWkWarps>(sm.cnt, sm.off, sm.gofs, &sm.total, a.nbins, a.wcnt, a.wcap, a.trash_at, a.overflow);
+    Resv rsv;
+    scan_reserve<kWkWarps>(sm.cnt, sm.off, &sm.total, a.nbins, a.wcnt, rsv);
     __syncthreads();
     {
       const uint32_t off_a = smem_addr(sm.off), srt_a = smem_addr(sm.srt), sbin_a = smem_addr(sm.sbin);
@@ -2007,10 +2028,8 @@ __global__ void __launch_bounds__(kWkWarps * 32) k_far_walk(const FarWalkArgs a)
         asm volatile("st.shared.u8 [%0], %1;" : : "r"(sbin_a + k), "r"(b) : "memory");
       }
     }
-    for (uint32_t b = tid; b < a.nbins; b += NT) {
-      if (sm.cnt[b]) sm.gofs[b] -= sm.off[b];
-      sm.cnt[b] = 0;
-    }
+    reserve_finish<kWkWarps>(rsv, sm.off, sm.gofs, a.wcap, a.trash_at, a.overflow);
+    for (uint32_t b = tid; b < a.nbins; b += NT) sm.cnt[b] = 0;
     __syncthreads();
     const uint32_t total = sm.total;
     for (uint32_t i = tid; i < total; i += NT) a.wbuf[sm.gofs[sm.sbin[i]] + i] = sm.srt[i];
